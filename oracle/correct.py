@@ -1,0 +1,258 @@
+"""fp64 oracle: mismatch statistics and TIS / RS corrections (TEST INFRASTRUCTURE ONLY).
+
+Real-number semantics from PAPER.md:
+  delta_t = log pi_train_old - log pi_rollout_old            (§2)
+  r_corr  = pi_train_old / pi_rollout_old = e^delta          (§4.2)
+  TIS weight  w_t = min(r_corr,t, tau_tok)                   (L_TIS)
+  K1(r) = -log r,  K3(r) = (r - 1) - log r                   (§4.1)
+  S_seq(q_1:T) = sum_t K(q_t), K in {K1, K3}                 (§4.2)
+  sequence keep  1[S_seq <= tau_seq]                          (L_RS; App. A.4)
+  tau_tok = 2, tau_seq = 0.001 in the paper's runs
+
+Because integer outputs (masks, counts) must be bit-exact between this oracle
+and the GPU, they are defined by the decision-path arithmetic contract of
+SURVEY.md §8(c) C.3, which is written out here step by step.  Every floating
+operation below is ONE IEEE binary64 round-to-nearest numpy ufunc (no fused
+multiply-add: numpy never fuses separate ufunc calls).
+
+  C.3.1  delta = (double)lp_num - (double)lp_den
+  C.3.2  non-finite delta -> data error carrying the first bad (global) index
+  C.3.3  threshold tests in the log domain on delta:
+           truncated  <=> delta > ln tau_tok
+           token keep <=> ln lo <= delta <= ln hi               (reading U4)
+  C.3.5  K1 = -delta
+  C.3.6  K3 = k3_c(delta): |delta| <= 1: delta^2 * P(delta), P the Horner
+         series of (e^x - 1 - x)/x^2 with coefficients RN(1/n!), n = 2..23;
+         otherwise (exp_c(delta) - 1) - delta, exp_c = Cody-Waite reduction
+         k = rint(delta * log2 e), r = (delta - k*ln2_hi) - k*ln2_lo, degree-13
+         Taylor Horner on r, then ldexp(., k); exp_c = +inf for delta > 709,
+         0 for delta < -700.
+  C.3.7  w = (float)(truncated ? tau_tok : min(exp_c(delta), tau_tok))
+  C.3.8  fixed point X = rint(K * 2^52) (ties to even); |K| > 2^10 (or
+         non-finite) saturates X = sign(K) * 2^62 and counts as saturated.
+         Sums are exact Python integers.
+  C.3.9  sequence keep: no saturated token and
+           SUM : X_s <= floor(tau_seq * 2^52)
+           MEAN: X_s <= floor(tau_seq * 2^52 * T_s)
+         (T_s = contributing response tokens; T_s == 0 -> keep).  The floor is
+         taken exactly with fractions.Fraction.
+  C.3.10 statistics = exact integer totals; means = float(total) * 2^-52 / count.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+from fractions import Fraction
+
+import numpy as np
+
+# ---- constants of the contract (each the correctly rounded binary64 value) ----
+LOG2E = float.fromhex("0x1.71547652b82fep+0")       # RN(1/ln 2)
+LN2_HI = float.fromhex("0x1.62e42fee00000p-1")      # ln 2 split (fdlibm), hi has 32 zero low bits
+LN2_LO = float.fromhex("0x1.a39ef35793c76p-33")
+INV_FACT = [float(Fraction(1, math.factorial(n))) for n in range(0, 24)]  # RN(1/n!)
+FX_SCALE = 2.0 ** 52
+SAT_K = 2.0 ** 10
+SAT_X = 2 ** 62
+
+SEQ_NONE, SEQ_K1, SEQ_K3 = 0, 1, 3
+AGG_SUM, AGG_MEAN = 0, 1
+
+
+class DataError(ValueError):
+    """Non-finite log-prob (TIM_ERR_DATA analogue); .index is the first bad global index."""
+
+    def __init__(self, index: int):
+        super().__init__(f"non-finite delta at token {index}")
+        self.index = index
+
+
+@dataclasses.dataclass
+class Cfg:
+    tis: bool = False
+    tis_cap: float = 2.0
+    log_tis_cap: float = math.log(2.0)
+    tok_rs: bool = False
+    log_tok_lo: float = -math.log(2.0)
+    log_tok_hi: float = math.log(2.0)
+    seq_rs: int = SEQ_NONE
+    seq_agg: int = AGG_SUM
+    tau_seq: float = 1e-3
+
+
+def delta(lp_num, lp_den) -> np.ndarray:
+    """C.3.1: one rounded subtraction of the widened fp32 inputs."""
+    return np.asarray(lp_num, dtype=np.float32).astype(np.float64) - \
+        np.asarray(lp_den, dtype=np.float32).astype(np.float64)
+
+
+def exp_contract(d) -> np.ndarray:
+    """C.3.6 exp_c: Cody-Waite reduction + degree-13 Taylor Horner + ldexp."""
+    d = np.asarray(d, dtype=np.float64)
+    dd = np.where(np.isfinite(d), np.clip(d, -700.0, 709.0), 0.0)
+    k = np.rint(dd * LOG2E)
+    r = (dd - k * LN2_HI) - k * LN2_LO
+    p = np.full_like(r, INV_FACT[13])
+    for n in range(12, -1, -1):
+        p = p * r + INV_FACT[n]
+    out = np.ldexp(p, k.astype(np.int64))
+    out = np.where(d > 709.0, np.inf, out)
+    out = np.where(d < -700.0, 0.0, out)
+    return out
+
+
+def k3_contract(d) -> np.ndarray:
+    """C.3.6 K3 = e^d - 1 - d: series branch for |d| <= 1, exp branch otherwise."""
+    d = np.asarray(d, dtype=np.float64)
+    small = np.abs(d) <= 1.0
+    ds = np.where(small, d, 0.0)
+    P = np.full_like(ds, INV_FACT[23])
+    for n in range(22, 1, -1):
+        P = P * ds + INV_FACT[n]
+    series = (ds * ds) * P
+    big = (exp_contract(d) - 1.0) - d
+    return np.where(small, series, big)
+
+
+def fixed_point(K) -> tuple[np.ndarray, np.ndarray]:
+    """C.3.8: X = rint(K * 2^52) as int64; |K| > 2^10 or non-finite -> +-2^62, saturated."""
+    K = np.asarray(K, dtype=np.float64)
+    sat = ~(np.abs(K) <= SAT_K)
+    Ks = np.where(sat, 0.0, K)
+    X = np.rint(Ks * FX_SCALE).astype(np.int64)
+    sgn = np.where(np.signbit(K), -1, 1).astype(np.int64)
+    X = np.where(sat, sgn * np.int64(SAT_X), X)
+    return X, sat
+
+
+def _isum(x: np.ndarray) -> int:
+    """Exact integer sum (Python ints)."""
+    return int(sum(int(v) for v in x.tolist()))
+
+
+def seq_threshold(tau: float, T: int, agg: int) -> int:
+    """C.3.9 exact floor(tau * 2^52 * (T if MEAN else 1))."""
+    f = Fraction(tau) * (2 ** 52) * (T if agg == AGG_MEAN else 1)
+    return math.floor(f)
+
+
+def local_partials(lp_num, lp_den, cu_seqlens, cfg: Cfg, resp_mask=None, tok_begin: int = 0):
+    """Pass 1 on one shard [tok_begin, tok_begin + n): per-token outputs and the exact
+    per-sequence / global integer partials that one rank contributes."""
+    cu = np.asarray(cu_seqlens, dtype=np.int64)
+    S = cu.size - 1
+    d = delta(lp_num, lp_den)
+    n = d.size
+    bad = ~np.isfinite(d)
+    if bad.any():
+        raise DataError(tok_begin + int(np.argmax(bad)))
+    resp = np.ones(n, bool) if resp_mask is None else (np.asarray(resp_mask) != 0)
+    trunc = (d > cfg.log_tis_cap) if cfg.tis else np.zeros(n, bool)
+    if cfg.tis:
+        w64 = np.where(trunc, cfg.tis_cap, np.minimum(exp_contract(d), cfg.tis_cap))
+        w = w64.astype(np.float32)
+    else:
+        w = np.ones(n, np.float32)
+    keep = ((cfg.log_tok_lo <= d) & (d <= cfg.log_tok_hi)) if cfg.tok_rs else np.ones(n, bool)
+    coeff = np.where(resp & keep, w, np.float32(0.0)).astype(np.float32)
+
+    k1 = -d
+    k3 = k3_contract(d)
+    X_abs, _ = fixed_point(np.abs(d))
+    X_k1, _ = fixed_point(k1)
+    X_k3, _ = fixed_point(k3)
+    glob = {
+        "n_tok": n,
+        "n_resp_tok": int(resp.sum()),
+        "n_truncated": int((resp & trunc).sum()),
+        "n_tok_rejected": int((resp & ~keep).sum()),
+        "n_saturated": 0,
+        "max_abs_delta": float(np.abs(d[resp]).max()) if resp.any() else 0.0,
+        "sum_abs_delta": _isum(X_abs[resp]),
+        "sum_k1": _isum(X_k1[resp]),
+        "sum_k3": _isum(X_k3[resp]),
+    }
+    seq = np.zeros((S, 3), dtype=object)  # (X_s, T_s, nsat_s) Python ints
+    seq[:] = 0
+    if cfg.seq_rs != SEQ_NONE:
+        Xq, satq = fixed_point(k1 if cfg.seq_rs == SEQ_K1 else k3)
+        contrib = resp & keep
+        glob["n_saturated"] = int((contrib & satq).sum())
+        g0, g1 = tok_begin, tok_begin + n
+        for s in range(S):
+            a, b = max(int(cu[s]), g0), min(int(cu[s + 1]), g1)
+            if a >= b:
+                continue
+            sl = slice(a - g0, b - g0)
+            c = contrib[sl]
+            seq[s, 0] = _isum(Xq[sl][c])
+            seq[s, 1] = int(c.sum())
+            seq[s, 2] = int((satq[sl] & c).sum())
+    tokens = {"delta": d, "tis_w": w, "tok_keep": keep.astype(np.uint8), "coeff_prov": coeff}
+    return tokens, glob, seq
+
+
+def combine(parts):
+    """Exact combination of the (glob, seq) partials of all ranks (order-free: integers / max)."""
+    globs = [g for g, _ in parts]
+    out = {k: sum(g[k] for g in globs) for k in globs[0] if k != "max_abs_delta"}
+    out["max_abs_delta"] = max(g["max_abs_delta"] for g in globs)
+    seq = parts[0][1].copy()
+    for _, s in parts[1:]:
+        seq = seq + s
+    return out, seq
+
+
+def decide(seq, cfg: Cfg):
+    """C.3.9: per-sequence keep flags and scores from the combined exact partials."""
+    S = seq.shape[0]
+    keep = np.ones(S, np.uint8)
+    score = np.zeros(S, np.float64)
+    if cfg.seq_rs == SEQ_NONE:
+        return keep, score
+    for s in range(S):
+        X, T, nsat = int(seq[s, 0]), int(seq[s, 1]), int(seq[s, 2])
+        sc = float(X) * (2.0 ** -52)
+        if cfg.seq_agg == AGG_MEAN:
+            sc = sc / T if T > 0 else 0.0
+        score[s] = sc
+        if T == 0:
+            keep[s] = 1
+        elif nsat > 0:
+            keep[s] = 0
+        else:
+            keep[s] = 1 if X <= seq_threshold(cfg.tau_seq, T, cfg.seq_agg) else 0
+    return keep, score
+
+
+def finalize_stats(glob, seq_keep, n_seq: int):
+    """C.3.10: host-side statistics from exact totals."""
+    st = dict(glob)
+    st["n_seq"] = n_seq
+    st["n_seq_rejected"] = int((np.asarray(seq_keep) == 0).sum())
+    n = glob["n_resp_tok"]
+    for k in ("abs_delta", "k1", "k3"):
+        st["mean_" + k] = (float(glob["sum_" + k]) * (2.0 ** -52)) / n if n else 0.0
+    return st
+
+
+def seq_index(cu_seqlens, tok_begin: int, n: int) -> np.ndarray:
+    """Sequence id of every local token (searchsorted on the global offsets)."""
+    cu = np.asarray(cu_seqlens, dtype=np.int64)
+    g = np.arange(tok_begin, tok_begin + n, dtype=np.int64)
+    return np.searchsorted(cu, g, side="right") - 1
+
+
+def correct(lp_num, lp_den, cu_seqlens, cfg: Cfg, resp_mask=None):
+    """Single-shard (P = 1) end-to-end oracle: returns a dict with every output."""
+    tokens, glob, seq = local_partials(lp_num, lp_den, cu_seqlens, cfg, resp_mask, 0)
+    glob, seq = combine([(glob, seq)])
+    seq_keep, score = decide(seq, cfg)
+    sid = seq_index(cu_seqlens, 0, tokens["delta"].size)
+    coeff = np.where(seq_keep[sid] != 0, tokens["coeff_prov"], np.float32(0.0)).astype(np.float32)
+    stats = finalize_stats(glob, seq_keep, seq.shape[0])
+    return {
+        "delta": tokens["delta"], "tis_w": tokens["tis_w"], "tok_keep": tokens["tok_keep"],
+        "seq_keep": seq_keep, "seq_score": score, "coeff": coeff, "stats": stats,
+        "seq_partials": seq,
+    }
