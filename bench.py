@@ -1,0 +1,405 @@
+"""bench.py -- throughput of the batch-invariant log-prob + TIS/RS hot path on B200.
+
+    python bench.py [--gpus N --steps K --warmup W --config c1 --impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+One step = one pass of the whole hot path over one batch:
+tim_logprob (lm_head GEMM + fused online log-softmax / gather / entropy + slice merge) on the
+rank's tokens, then tim_correct (delta, TIS, sequence-RS K3 with the paper's tau values,
+statistics; NCCL all-gather of exact partials when N > 1).  Weak scaling: every rank scores
+its own C1-shaped batch (64 sequences x 4096 tokens); value = all ranks' tokens / max-rank time.
+
+Metric (BASELINE.json): logprob tokens/sec at V = 151936; also max |dlogp| across batch shapes.
+Inputs are synthetic (synth/), resident in HBM for `value`; `e2e` re-times the step through the
+public API from pinned host buffers (H2D of the inputs and D2H of the results inside the timing).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+KERNELS_PER_STEP = 5  # logprob fwd + merge, correct local + finish + zero
+
+
+def _peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return p, "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return dict(FALLBACK_PEAKS), "fallback (B200_PROFILING.md)"
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "200"], stdout=open(self.path, "w"),
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                rows.append(f)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def _traffic():
+    """dram bytes per launch of the logprob kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_logprob_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch_c1")
+    except Exception:
+        return None
+
+
+def build_workload(cfg, rank, device):
+    seed = cfg.seed + 1000 * rank
+    W = synth.head_weight(cfg.vocab, cfg.hidden, cfg.seed, device=device)  # replicated lm_head
+    ids = synth.token_ids(cfg.n_tok, cfg.vocab, seed, device=device)
+    H = synth.hidden_states(cfg.n_tok, cfg.hidden, seed, device=device, weight=W, ids=ids, mode="peaked")
+    return W, H, ids
+
+
+def run_ours(args):
+    from paper_2605_14220_b200 import tim
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = synth.CONFIGS[args.config]
+    W, H, ids = build_workload(cfg, rank, dev)
+    N = cfg.n_tok
+    S_local = cfg.n_seq
+    # global sequence offsets: every rank owns S_local whole sequences of the global batch
+    cu = synth.cu_seqlens(S_local * world, cfg.seq_len).to(dev)
+    mask = synth.resp_mask(synth.cu_seqlens(S_local, cfg.seq_len), cfg.prompt_len).to(dev)
+    tok_begin = rank * N
+    comm = tim.Comm() if world > 1 else None
+    ccfg = tim.PRESETS["tis-srs-k3-corr-ratio"]
+
+    # rollout-side log-probs: the same head with a P3 perturbation (setup, untimed)
+    lp0, _ = tim.logprob(H, W, ids)
+    lp_roll = synth.perturb_laplace_mix(lp0, cfg.seed + rank)
+    lp = torch.empty(N, dtype=torch.float32, device=dev)
+    ent = torch.empty(N, dtype=torch.float32, device=dev)
+    S_glob = cu.numel() - 1
+    cout = {"tis_w": torch.empty(N, dtype=torch.float32, device=dev),
+            "tok_keep": torch.empty(N, dtype=torch.uint8, device=dev),
+            "seq_keep": torch.empty(S_glob, dtype=torch.uint8, device=dev),
+            "coeff": torch.empty(N, dtype=torch.float32, device=dev),
+            "seq_score": torch.empty(S_glob, dtype=torch.float64, device=dev),
+            "stats_raw": torch.zeros(tim.STATS_BYTES, dtype=torch.uint8, device=dev)}
+    status = tim.new_status(dev)
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record()
+        tim.logprob(H, W, ids, out=(lp, ent), status=status)
+        if ev is not None:
+            ev[1].record()
+        tim.correct(lp, lp_roll, cu, ccfg, mask, tok_begin=tok_begin, comm=comm, status=status,
+                    return_stats=False, out=cout)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t0.record()
+    for k in range(args.steps):
+        step(evs[k])
+    t1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    lp_ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    if world > 1:
+        t = torch.tensor([ms, lp_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms, lp_ms = t.tolist()
+    code, first = tim.read_status(status)
+    assert code == 0, f"device status {code} at {first}"
+    stats = tim.stats_from_bytes(cout["stats_raw"])
+
+    # invariance (untimed): a sample of rows re-scored alone and in other pack sizes, bitwise
+    samp = torch.arange(0, N, max(1, N // 64), device=dev)[:64]
+    ref_bits = lp[samp].view(torch.int32)
+    max_shape_diff = 0.0
+    for r in samp[:16].tolist():
+        a, _ = tim.logprob(H[r:r + 1], W, ids[r:r + 1])
+        max_shape_diff = max(max_shape_diff, abs(a.item() - lp[r].item()))
+    a, _ = tim.logprob(H[samp], W, ids[samp])
+    if not torch.equal(a.view(torch.int32), ref_bits):
+        max_shape_diff = max(max_shape_diff, (a - lp[samp]).abs().max().item())
+
+    # end to end through the public API from pinned host buffers
+    e2e = None
+    if args.e2e_steps > 0:
+        Hh = H.cpu().pin_memory()
+        idsh = ids.cpu().pin_memory()
+        rollh = lp_roll.cpu().pin_memory()
+        maskh = mask.cpu().pin_memory()
+        cuh = cu.cpu().pin_memory()
+        del H
+        torch.cuda.empty_cache()
+
+        def e2e_step():
+            lph, enth = tim.logprob(Hh, W, idsh, device=dev)
+            res = tim.correct(lph, rollh, cuh, ccfg, maskh, tok_begin=tok_begin, comm=comm, device=dev)
+            return lph, enth, res
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.e2e_steps):
+            lph, enth, res = e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ems = t.item()
+        h2d = Hh.numel() * 2 + idsh.numel() * 8 + 2 * N * 4 + maskh.numel() + cuh.numel() * 8
+        d2h = 2 * N * 4 + N * 4 + N + S_glob + N * 4 + S_glob * 8 + tim.STATS_BYTES
+        e2e = {"value": world * N * args.e2e_steps / (ems / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+               "ms_per_step": ems / args.e2e_steps}
+
+    peaks, peak_src = _peaks()
+    flop = 2.0 * cfg.vocab * cfg.hidden * N
+    achieved = flop / (lp_ms / 1e3) / 1e12
+    peak = float(peaks["bf16_tflops_sustained"])
+    out = {
+        "metric": "logprob tokens/sec at V=151936 (1/2/4/8 B200); max |dlogp| across batch shapes",
+        "value": world * N * args.steps / (ms / 1e3),
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16 inputs, fp32 tensor-core accumulate (tcgen05 kind::f16); fp64 correction",
+        "data": "synthetic (synth/: peaked-mode hidden states, N(0,0.02^2) head, seeded)",
+        "config": {
+            "workload": f"{cfg.name}: Qwen3-shaped lm_head d={cfg.hidden}, V={cfg.vocab}, {cfg.n_seq} seqs x "
+                        f"{cfg.seq_len} tokens per GPU; logprob + entropy + tis-srs-k3-corr-ratio correction",
+            "hidden": cfg.hidden, "vocab": cfg.vocab, "n_seq_per_gpu": cfg.n_seq, "seq_len": cfg.seq_len,
+            "tokens_per_gpu": N, "global_batch_tokens": world * N, "parallelism": f"dp{world} (token-sharded)",
+            "l2": "inputs larger than L2 (H %.2f GB/GPU, W %.2f GB)" % (H_bytes(cfg) / 1e9, W.numel() * 2 / 1e9),
+        },
+        "max_abs_dlogp_across_shapes": max_shape_diff,
+        "gpu_launches": KERNELS_PER_STEP * args.steps,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "frac_of_burst": achieved / float(peaks["bf16_tflops"]),
+                     "peak_source": peak_src + " bf16_tflops_sustained", "traffic": _traffic(),
+                     "kernel": "tim_logprob (tcgen05 GEMM + fused epilogue + slice merge)",
+                     "kernel_ms": lp_ms, "algorithmic_flop_per_token": 2 * cfg.vocab * cfg.hidden},
+        "clocks": clk,
+        "e2e": e2e,
+        "correction_stats": {k: stats[k] for k in ("n_resp_tok", "n_truncated", "n_seq_rejected", "max_abs_delta",
+                                                     "mean_abs_delta", "mean_k3")},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"], out["max_abs_dlogp_vs_oracle"] = cpu_baseline(cfg, W, ids, lp, lp_roll, mask, dev,
+                                                                            args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def H_bytes(cfg):
+    return cfg.n_tok * cfg.hidden * 2
+
+
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max((i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"), default=1)
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(cfg, W, ids, lp_gpu, lp_roll, mask, dev, seconds):
+    """The fp64 oracle as it stands, on the host cores, over a bounded sample of the workload."""
+    import math
+
+    import numpy as np
+
+    from oracle import correct as oc
+    from oracle.logprob import logprob_entropy
+
+    N = cfg.n_tok
+    Wc = W.cpu()
+    rows = torch.randperm(N, generator=torch.Generator().manual_seed(3))[:4096]
+    Hs = synth.hidden_states(N, cfg.hidden, cfg.seed, device=dev, weight=W, ids=ids, mode="peaked")
+    done, t_lp, dmax = 0, 0.0, 0.0
+    while t_lp < seconds * 0.6 and done < rows.numel():
+        r = rows[done:done + 32]
+        rd = r.to(dev)
+        h = Hs[rd].cpu()
+        t = time.perf_counter()
+        olp, _ = logprob_entropy(h, Wc, ids[rd].cpu(), row_chunk=32)
+        t_lp += time.perf_counter() - t
+        dmax = max(dmax, float(np.abs(lp_gpu[rd].cpu().double().numpy() - olp).max()))
+        done += r.numel()
+    del Hs
+    # correction oracle on whole sequences of the same batch
+    ocfg = oc.Cfg(tis=True, tis_cap=2.0, log_tis_cap=math.log(2.0), seq_rs=oc.SEQ_K3, seq_agg=oc.AGG_SUM,
+                  tau_seq=1e-3)
+    n_corr = min(N, cfg.seq_len * 8)
+    cu = synth.cu_seqlens(n_corr // cfg.seq_len, cfg.seq_len).numpy()
+    t = time.perf_counter()
+    oc.correct(lp_gpu[:n_corr].cpu().numpy(), lp_roll[:n_corr].cpu().numpy(), cu, ocfg, mask[:n_corr].cpu().numpy())
+    t_corr = time.perf_counter() - t
+    per_tok = t_lp / done + t_corr / n_corr
+    return ({"value": 1.0 / per_tok, "unit": "tokens/s", "cores": _blas_threads(), "kind": "oracle",
+             "sample": f"fp64 numpy oracle: logprob+entropy on {done} random rows of the {cfg.name} batch "
+                       f"({t_lp:.1f} s) + correction (tis-srs-k3) on {n_corr} tokens ({t_corr:.1f} s); "
+                       f"host {os.cpu_count()} logical cpus"}, dmax)
+
+
+def run_reference(args):
+    """--impl reference: the fp64 CPU oracle (this tier's reference arm) on the host cores."""
+    world, rank, _ = _dist()
+    if rank != 0:
+        return
+    import math
+
+    import numpy as np
+
+    from oracle import correct as oc
+    from oracle.logprob import logprob_entropy
+
+    cfg = synth.CONFIGS[args.config]
+    W = synth.head_weight(cfg.vocab, cfg.hidden, cfg.seed)
+    n_s = 32
+    ocfg = oc.Cfg(tis=True, tis_cap=2.0, log_tis_cap=math.log(2.0), seq_rs=oc.SEQ_K3, seq_agg=oc.AGG_SUM,
+                  tau_seq=1e-3)
+
+    def step(k):
+        ids = synth.token_ids(n_s, cfg.vocab, cfg.seed + k)
+        H = synth.hidden_states(n_s, cfg.hidden, cfg.seed + k, weight=W, ids=ids, mode="peaked")
+        t = time.perf_counter()
+        lp, _ = logprob_entropy(H, W, ids, row_chunk=32)
+        roll = lp + np.random.default_rng(k).laplace(0, 2e-3, n_s)
+        oc.correct(lp.astype(np.float32), roll.astype(np.float32), np.array([0, n_s]), ocfg)
+        return time.perf_counter() - t
+
+    for k in range(args.warmup):
+        step(k)
+    tot = sum(step(args.warmup + k) for k in range(args.steps))
+    v = n_s * args.steps / tot
+    out = {"impl": "reference", "metric": "logprob tokens/sec at V=151936 (1/2/4/8 B200); max |dlogp| across batch shapes",
+           "value": v, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic (synth/)",
+           "config": {"workload": f"{cfg.name}: d={cfg.hidden}, V={cfg.vocab}; {n_s}-token sample per step",
+                      "hidden": cfg.hidden, "vocab": cfg.vocab},
+           "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": _blas_threads(), "kind": "oracle",
+                            "sample": f"{n_s} tokens per step through the fp64 oracle (logprob + entropy + "
+                                      f"tis-srs-k3 correction)"},
+           "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c1", choices=["c1", "c2", "c3", "toy"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

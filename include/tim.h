@@ -1,0 +1,246 @@
+/*
+ * tim.h -- C ABI of the B200-native batch-invariant log-prob + TIS/RS library (libtim.so).
+ *
+ * Method: arxiv 2605.14220 ("Training-Inference Mismatch", PAPER.md).  The
+ * library implements the data-parallel hot path of the paper's zero-mismatch
+ * setting:
+ *   tim_logprob         per-token log pi(a_t | s_t) of the sampled id and the entropy,
+ *                       recomputed from the final hidden state (§4.1
+ *                       "the trainer re-evaluates the sampled tokens"; §2 P:99 the
+ *                       token distributions), bit-identical for a token whatever batch
+ *                       it is scored in (§3.1 P:202-207 "fix the tiling and reduction
+ *                       order").
+ *   tim_mismatch_stats  delta_t = log pi_train_old - log pi_rollout_old (§2),
+ *                       batch mean / max |delta| (fig:delta_t_batch), K1 / K3
+ *                       means (§4.1).
+ *   tim_correct         TIS weights min(r_corr, tau_tok) (§4.2), token-level
+ *                       RS (reading U4), sequence-level RS 1[S_seq <= tau_seq] with
+ *                       S_seq = sum_t K(q_t) (App. A.4), the
+ *                       per-token coefficient resp * tok_keep * seq_keep * w.
+ *
+ * Conventions (apply to every entry point unless stated otherwise)
+ *   - Every pointer argument is DEVICE memory owned by the caller, except
+ *     `cfg_host` (host) and the tim_stats_finalize argument (host).  The library
+ *     allocates nothing on the hot path; the only library-owned object is tim_comm.
+ *   - All calls are asynchronous and stream-ordered on `stream` (cudaStream_t passed
+ *     as void*; NULL = legacy default stream).  Collectives are enqueued on it too.
+ *   - Argument errors are detected on the host and returned synchronously BEFORE any
+ *     launch (nothing is enqueued).  Data errors found on the device (token id out of
+ *     [0, V), non-finite log-prob) are reported in the caller's device status word
+ *     `dstatus` (zero-initialise it; code = TIM_ERR_DATA, first_bad_index = minimum
+ *     offending global token index, written with integer atomics => deterministic).
+ *   - Runs on sm_100a only; on any other device every compute call returns
+ *     TIM_ERR_UNSUPPORTED.  There is no CPU fallback.
+ *   - A tim_comm must not be used from two host threads at once (NCCL rule).
+ */
+#ifndef TIM_H_
+#define TIM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TIM_ABI_VERSION 1
+
+typedef enum {
+  TIM_OK = 0,
+  TIM_ERR_NULL = 1,        /* a required pointer is NULL                                  */
+  TIM_ERR_SHAPE = 2,       /* a size is out of range / inconsistent                       */
+  TIM_ERR_ALIGN = 3,       /* TMA alignment: pointers 16-B aligned, ld_hidden*2 % 16 == 0 */
+  TIM_ERR_VALUE = 4,       /* a scalar parameter is out of range (temperature, tau, ...)  */
+  TIM_ERR_WORKSPACE = 5,   /* workspace too small (query the *_workspace_bytes function)  */
+  TIM_ERR_CUDA = 6,        /* a CUDA runtime / driver call failed                         */
+  TIM_ERR_NCCL = 7,        /* NCCL unavailable or a collective failed                     */
+  TIM_ERR_UNSUPPORTED = 8, /* device is not sm_100 (B200)                                 */
+  TIM_ERR_DATA = 9         /* device-side data error (only ever stored in dstatus->code)   */
+} tim_status;
+
+/* Device status word: caller-owned device memory, zero-initialised by the caller. */
+typedef struct {
+  int32_t code;             /* TIM_OK or TIM_ERR_DATA                                */
+  int32_t reserved;
+  int64_t first_bad_index;  /* valid when code != 0: minimum offending token index    */
+} tim_device_status;
+
+const char* tim_status_string(tim_status s);
+int tim_abi_version(void);
+
+/* ----------------------------------------------------------------------------
+ * tim_logprob
+ *
+ * For every token row t in [0, n_tok):
+ *   z_v   = sum_k H[t,k] W[v,k]                 bf16 x bf16 products, fp32 accumulation
+ *                                               (tcgen05, never rounded to bf16, reading U8)
+ *   x_v   = z_v / T_t                           T_t = temperatures[t] if given, else temperature (U7)
+ *   logp  = x_{ids[t]} - log sum_v exp(x_v)     natural log, all V rows count (U10)
+ *   H_t   = -sum_v p_v ln p_v                   entropy in nats of the tempered distribution (U9)
+ * Row t is paired with ids[t]: the next-token shift is the caller's job (U18).
+ *
+ * Batch invariance: every reduction has a split and order that depends only on
+ * (V, hidden) -- never on n_tok, the row's position in the batch, the number of
+ * SMs or of GPUs -- so a token's logp/entropy bits are identical whether it is
+ * scored alone or in any packed batch (§3.1).
+ *
+ * Layout / ownership:
+ *   hidden_bf16  [n_tok, hidden] row stride ld_hidden elements (>= hidden); 16-B aligned;
+ *                ld_hidden*2 % 16 == 0.  bf16 (uint16 storage).
+ *   weight_bf16  [vocab, hidden] contiguous, 16-B aligned (the lm_head weight, K-major).
+ *   token_ids    [n_tok] int64; ids outside [0, vocab) -> dstatus TIM_ERR_DATA, logp NaN.
+ *   temperatures_or_null [n_tok] fp32 (> 0, finite) or NULL.
+ *   logp_out     [n_tok] fp32.  entropy_out_or_null [n_tok] fp32 or NULL.
+ *   workspace    >= tim_logprob_workspace_bytes(n_tok, hidden, vocab) bytes, 256-B aligned.
+ * Constraints: hidden % 64 == 0, 64 <= hidden <= 16384; 1 <= vocab <= 2^24;
+ *   0 <= n_tok < 2^31; temperature > 0 and finite.  n_tok == 0 -> TIM_OK, no launch.
+ * Errors: TIM_ERR_NULL / SHAPE / ALIGN / VALUE / WORKSPACE (sync, nothing launched),
+ *   TIM_ERR_UNSUPPORTED (not sm_100), TIM_ERR_CUDA (launch failure).
+ * -------------------------------------------------------------------------- */
+size_t tim_logprob_workspace_bytes(int64_t n_tok, int32_t hidden, int32_t vocab);
+tim_status tim_logprob(const void* hidden_bf16, int64_t ld_hidden,
+                       const void* weight_bf16, int32_t hidden, int32_t vocab,
+                       const int64_t* token_ids, int64_t n_tok,
+                       float temperature, const float* temperatures_or_null,
+                       float* logp_out, float* entropy_out_or_null,
+                       void* workspace, size_t workspace_bytes,
+                       tim_device_status* dstatus, void* stream);
+
+/* Number of vocab slices S_v of the fixed split for a given vocab (numerics contract, U20). */
+int32_t tim_logprob_vocab_slices(int32_t vocab);
+
+/* ----------------------------------------------------------------------------
+ * Corrections and statistics
+ *
+ * Inputs common to tim_mismatch_stats / tim_correct / tim_correct_local:
+ *   logp_num, logp_den  [n_tok_local] fp32; delta = (double)num - (double)den (C.3.1).
+ *                       (num, den) = (train_old, rollout) gives r_corr = e^delta;
+ *                       (cur, rollout) gives r^rollout_ppo as masking signal q_t.
+ *   cu_seqlens_global   [n_seq + 1] int64 global sequence offsets, cu[0] == 0, non-decreasing.
+ *   tok_begin           global index of this rank's first token; this rank holds tokens
+ *                       [tok_begin, tok_begin + n_tok_local) which must lie in [0, cu[n_seq]].
+ *                       Sequences may straddle ranks.
+ *   resp_mask_or_null   [n_tok_local] u8 (1 = response token); NULL = all response (U11).
+ * Only response tokens enter K sums, T_s and statistics; non-response tokens get coeff 0.
+ * -------------------------------------------------------------------------- */
+typedef enum { TIM_SEQ_NONE = 0, TIM_SEQ_K1 = 1, TIM_SEQ_K3 = 3 } tim_seq_rs;
+typedef enum { TIM_AGG_SUM = 0, TIM_AGG_MEAN = 1 } tim_agg;
+
+/* Correction configuration (host memory).  No defaults: the caller sets every field.
+ * Paper values: tis_cap = 2, log_tis_cap = ln 2, tau_seq = 0.001. */
+typedef struct {
+  int32_t tis;          /* 1: w = min(e^delta, tis_cap); truncated iff delta > log_tis_cap   */
+  int32_t tok_rs;       /* 1: token keep iff log_tok_lo <= delta <= log_tok_hi (U4)          */
+  int32_t seq_rs;       /* tim_seq_rs: sequence score K1 (= -delta) or K3 (C.3.6)            */
+  int32_t seq_agg;      /* tim_agg: S_s = sum (paper literal) or mean over contributing tokens */
+  double tis_cap;       /* tau_tok > 0, finite                                              */
+  double log_tis_cap;   /* ln tau_tok, computed by the caller (no libm on the decision path) */
+  double log_tok_lo;    /* ln lower ratio bound                                             */
+  double log_tok_hi;    /* ln upper ratio bound, >= log_tok_lo                              */
+  double tau_seq;       /* keep iff S_s <= tau_seq; |tau_seq| < 2^10, finite                 */
+} tim_correct_cfg;
+
+/* Statistics.  Device writes every integer field and max_abs_delta; the three means are
+ * filled by tim_stats_finalize on a host copy.  int128 values are {lo, hi} two's complement,
+ * scale 2^-52 (fixed point of C.3.8), exact and independent of sharding / GPU count. */
+typedef struct {
+  int64_t n_tok;            /* tokens scored (all ranks)                                   */
+  int64_t n_resp_tok;       /* response tokens                                             */
+  int64_t n_seq;
+  int64_t n_truncated;      /* response tokens with delta > log_tis_cap (when tis)          */
+  int64_t n_tok_rejected;   /* response tokens failing token-RS (when tok_rs)              */
+  int64_t n_seq_rejected;
+  int64_t n_saturated;      /* contributing tokens whose |K| > 2^10 (sequence rejected, U19) */
+  int64_t sum_abs_delta_fx[2];
+  int64_t sum_k1_fx[2];
+  int64_t sum_k3_fx[2];
+  double max_abs_delta;
+  double mean_abs_delta;    /* host: tim_stats_finalize                                    */
+  double mean_k1;
+  double mean_k3;
+} tim_stats;
+
+/* Pure host: fills the means of a host copy from its exact totals (RN conversions). */
+tim_status tim_stats_finalize(tim_stats* host_copy);
+
+size_t tim_correct_workspace_bytes(int64_t n_tok_local, int64_t n_seq, int32_t nranks);
+
+/* Statistics only (no masks).  comm_or_null: NULL for a single rank, else the NCCL
+ * communicator of all ranks sharing the batch (exact all-gather of integer partials). */
+typedef struct tim_comm tim_comm;
+tim_status tim_mismatch_stats(const float* logp_num, const float* logp_den,
+                              const int64_t* cu_seqlens_global, int64_t n_seq,
+                              int64_t tok_begin, int64_t n_tok_local,
+                              const uint8_t* resp_mask_or_null,
+                              tim_comm* comm_or_null, tim_stats* stats_dev,
+                              void* workspace, size_t workspace_bytes,
+                              tim_device_status* dstatus, void* stream);
+
+/* Full correction.  Outputs (device):
+ *   tis_w     [n_tok_local] fp32  w_t (tis) or 1.0
+ *   tok_keep  [n_tok_local] u8    token-RS keep (all 1 when !tok_rs)
+ *   seq_keep  [n_seq]       u8    sequence keep (all 1 when seq_rs == NONE)
+ *   coeff     [n_tok_local] fp32  resp * tok_keep * seq_keep * (tis ? w : 1)
+ *   seq_score_or_null [n_seq] f64 S_s (SUM) or S_s / T_s (MEAN) from the exact sum
+ *   stats_dev may be NULL.
+ */
+tim_status tim_correct(const float* logp_num, const float* logp_den,
+                       const int64_t* cu_seqlens_global, int64_t n_seq,
+                       int64_t tok_begin, int64_t n_tok_local,
+                       const uint8_t* resp_mask_or_null,
+                       const tim_correct_cfg* cfg_host, tim_comm* comm_or_null,
+                       float* tis_w, uint8_t* tok_keep, uint8_t* seq_keep, float* coeff,
+                       double* seq_score_or_null, tim_stats* stats_dev,
+                       void* workspace, size_t workspace_bytes,
+                       tim_device_status* dstatus, void* stream);
+
+/* ----------------------------------------------------------------------------
+ * Split form of tim_correct for callers that exchange partials themselves
+ * (e.g. torch.distributed).  tim_correct == local -> all-gather -> finish.
+ *
+ * tim_correct_local writes this rank's exact partial block (tim_correct_partial_bytes(n_seq)
+ * bytes at `partial_out`, device) and the per-token outputs tis_w, tok_keep and a
+ * provisional coeff (= resp * tok_keep * w).  The block is plain bytes: gather the blocks
+ * of all ranks contiguously, in rank order, into [nranks * partial_bytes] and pass them to
+ * tim_correct_finish on every rank.  finish sums the blocks exactly (int128), decides every
+ * sequence, zeroes coeff of this rank's tokens in rejected sequences, and writes seq_keep,
+ * seq_score and stats.  Block layout: tim_partial_header followed by n_seq tim_seq_partial.
+ * -------------------------------------------------------------------------- */
+typedef struct {
+  int64_t n_tok, n_resp_tok, n_truncated, n_tok_rejected, n_saturated;
+  uint64_t max_abs_delta_bits;       /* bits of a non-negative double (max commutes with bits) */
+  int64_t sum_abs_delta[2], sum_k1[2], sum_k3[2];
+  int64_t reserved[4];
+} tim_partial_header;                /* 128 B */
+typedef struct {
+  int64_t x_lo, x_hi;                /* int128 sum of X = rint(K * 2^52) over contributing tokens */
+  int64_t n_tok;                     /* T_s contribution                                          */
+  int64_t n_sat;                     /* saturated contributing tokens                             */
+} tim_seq_partial;                   /* 32 B */
+
+size_t tim_correct_partial_bytes(int64_t n_seq);
+tim_status tim_correct_local(const float* logp_num, const float* logp_den,
+                             const int64_t* cu_seqlens_global, int64_t n_seq,
+                             int64_t tok_begin, int64_t n_tok_local,
+                             const uint8_t* resp_mask_or_null, const tim_correct_cfg* cfg_host,
+                             float* tis_w, uint8_t* tok_keep, float* coeff,
+                             void* partial_out, tim_device_status* dstatus, void* stream);
+tim_status tim_correct_finish(const void* gathered_partials, int32_t nranks,
+                              const int64_t* cu_seqlens_global, int64_t n_seq,
+                              int64_t tok_begin, int64_t n_tok_local,
+                              const tim_correct_cfg* cfg_host,
+                              float* coeff, uint8_t* seq_keep, double* seq_score_or_null,
+                              tim_stats* stats_dev_or_null, void* stream);
+
+/* ----------------------------------------------------------------------------
+ * NCCL communicator (NVLink / NVSwitch).  libnccl.so.2 is loaded at run time.
+ * unique_id: 128 bytes from tim_comm_unique_id on rank 0, broadcast by the caller.
+ * -------------------------------------------------------------------------- */
+tim_status tim_comm_unique_id(void* unique_id_128B_out);
+tim_status tim_comm_init(const void* unique_id_128B, int32_t nranks, int32_t rank, tim_comm** out);
+tim_status tim_comm_destroy(tim_comm* comm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TIM_H_ */

@@ -1,0 +1,30 @@
+/*
+ * tim_debug.h -- TEST-ONLY entry points of libtim.so (GEMM bring-up and invariance tests).
+ * Not part of the product ABI; never called on the hot path.
+ */
+#ifndef TIM_DEBUG_H_
+#define TIM_DEBUG_H_
+
+#include "tim.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Same as tim_logprob (T = 1) but additionally writes the raw fp32 tcgen05 accumulators
+ * z[t, v] = sum_k H[t,k] W[v,k] to logits_out[t * ld_logits + v] (device, ld_logits >= vocab),
+ * so the TMA / UMMA-descriptor / TMEM layout can be checked against an fp64 matmul. */
+tim_status tim_debug_logprob_logits(const void* hidden_bf16, int64_t ld_hidden, const void* weight_bf16,
+                                    int32_t hidden, int32_t vocab, const int64_t* token_ids, int64_t n_tok,
+                                    float* logits_out, int64_t ld_logits, float* logp_out, float* entropy_out,
+                                    void* workspace, size_t workspace_bytes, void* stream);
+
+/* Process-global knobs: use_pair = 1 (default) selects the cta_group::2 kernel (the numerics
+ * contract), 0 the single-CTA cta_group::1 bring-up variant; max_ctas_or_clusters > 0 caps the
+ * persistent grid (emulates a GPU with fewer SMs for batch-invariance tests), 0 = all SMs. */
+tim_status tim_debug_set_kernel(int32_t use_pair, int32_t max_ctas_or_clusters);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,498 @@
+// api.cu -- the C ABI of libtim.so (include/tim.h): argument validation, workspace layout,
+// TMA tensor-map encoding, launch configuration, NCCL exchange, status mapping.
+// Every argument error returns synchronously before anything is enqueued.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/tim.h"
+#include "../../include/tim_debug.h"
+#include "tim_internal.h"
+
+using namespace tim;
+
+namespace {
+
+// ------------------------------------------------------------------ device --
+struct DevInfo {
+  bool ok = false;
+  bool sm100 = false;
+  int num_sms = 0;
+  int max_pair_clusters = 0;
+  int max_single_ctas = 0;
+};
+constexpr int kMaxDev = 64;
+DevInfo g_dev[kMaxDev];
+std::mutex g_mu;
+
+// debug knobs (tim_debug.h): kernel variant and an SM cap to emulate smaller GPUs
+int g_use_pair = 1;
+int g_max_clusters = 0;
+
+tim_status device_info(DevInfo** out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return TIM_ERR_CUDA;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevInfo& d = g_dev[dev];
+  if (!d.ok) {
+    int maj = 0, min = 0;
+    if (cudaDeviceGetAttribute(&maj, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return TIM_ERR_CUDA;
+    if (cudaDeviceGetAttribute(&min, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess) return TIM_ERR_CUDA;
+    if (cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return TIM_ERR_CUDA;
+    d.sm100 = (maj == 10 && min == 0);
+    d.max_pair_clusters = d.num_sms / 2;
+    d.max_single_ctas = d.num_sms;
+    d.ok = true;
+  }
+  *out = &d;
+  return d.sm100 ? TIM_OK : TIM_ERR_UNSUPPORTED;
+}
+
+// ------------------------------------------------------------- tensor maps --
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 [rows, cols] (cols contiguous), row pitch `pitch_elems`; box = 64 cols x box_rows, SW128
+bool encode_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t pitch_elems,
+                    uint32_t box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch_elems * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+
+constexpr int kMaxSlices = 8;
+inline int32_t n_vocab_tiles(int32_t vocab) { return (vocab + 255) / 256; }
+inline int32_t vocab_slices(int32_t vocab) {
+  const int32_t nvt = n_vocab_tiles(vocab);
+  return nvt < kMaxSlices ? nvt : kMaxSlices;
+}
+
+tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weight, int32_t d, int32_t vocab,
+                        const int64_t* ids, int64_t n_tok, float temperature, const float* temps, float* logp,
+                        float* ent, void* ws, size_t ws_bytes, tim_device_status* dstatus, void* stream,
+                        float* debug_logits, int64_t debug_ld) {
+  if (!weight) return TIM_ERR_NULL;
+  if (n_tok < 0 || n_tok >= (int64_t(1) << 31)) return TIM_ERR_SHAPE;
+  if (d < 64 || d > 16384 || d % 64 != 0) return TIM_ERR_SHAPE;
+  if (vocab < 1 || vocab > (1 << 24)) return TIM_ERR_SHAPE;
+  if (ld_hidden < d) return TIM_ERR_SHAPE;
+  if (!(temperature > 0.f) || !std::isfinite(temperature)) return TIM_ERR_VALUE;
+  if (!aligned(weight, 16) || (ld_hidden * 2) % 16 != 0) return TIM_ERR_ALIGN;
+  if (n_tok == 0) return TIM_OK;  // empty batch: pointers may be NULL, nothing is launched
+  if (!hidden || !ids || !logp) return TIM_ERR_NULL;
+  if (!aligned(hidden, 16)) return TIM_ERR_ALIGN;
+  if (!ws) return TIM_ERR_NULL;
+  if (!aligned(ws, 16)) return TIM_ERR_ALIGN;
+  if (ws_bytes < tim_logprob_workspace_bytes(n_tok, d, vocab)) return TIM_ERR_WORKSPACE;
+  DevInfo* dev = nullptr;
+  tim_status st = device_info(&dev);
+  if (st != TIM_OK) return st;
+
+  const bool pair = g_use_pair != 0;
+  CUtensorMap th, tw;
+  if (!encode_bf16_2d(&th, hidden, n_tok, d, ld_hidden, 128)) return TIM_ERR_CUDA;
+  if (!encode_bf16_2d(&tw, weight, vocab, d, d, fwd_w_box_rows(pair))) return TIM_ERR_CUDA;
+
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* wsb = static_cast<uint8_t*>(ws);
+  WsHeader* hdr = reinterpret_cast<WsHeader*>(wsb);
+  float4* partials = reinterpret_cast<float4*>(wsb + kWsHeaderBytes);
+  if (cudaMemsetAsync(hdr, 0, sizeof(WsHeader), s) != cudaSuccess) return TIM_ERR_CUDA;
+
+  LogprobParams p{};
+  p.ids = ids;
+  p.temps = temps;
+  p.temperature = temperature;
+  p.partials = partials;
+  p.n_tok = static_cast<int>(n_tok);
+  p.vocab = vocab;
+  p.hidden = d;
+  const int unit = fwd_unit_rows(pair);
+  p.n_mt = static_cast<int>((n_tok + unit - 1) / unit);
+  p.n_vt = n_vocab_tiles(vocab);
+  p.n_slices = vocab_slices(vocab);
+  p.debug_logits = debug_logits;
+  p.debug_ld = debug_ld;
+  const int64_t n_units = static_cast<int64_t>(p.n_mt) * p.n_slices;
+  int64_t ctas_cap = pair ? dev->max_pair_clusters : dev->max_single_ctas;
+  if (g_max_clusters > 0 && g_max_clusters < ctas_cap) ctas_cap = g_max_clusters;
+  const int64_t groups = n_units < ctas_cap ? n_units : ctas_cap;
+  const int grid = static_cast<int>(groups * (pair ? 2 : 1));
+  if (launch_logprob_fwd(pair, debug_logits != nullptr, th, tw, p, grid, s) != cudaSuccess) return TIM_ERR_CUDA;
+
+  MergeParams mp{};
+  mp.partials = partials;
+  mp.ids = ids;
+  mp.temps = temps;
+  mp.logp = logp;
+  mp.entropy = ent;
+  mp.n_tok = n_tok;
+  mp.vocab = vocab;
+  mp.n_slices = p.n_slices;
+  mp.ws = hdr;
+  mp.dstatus = dstatus;
+  if (launch_logprob_merge(mp, s) != cudaSuccess) return TIM_ERR_CUDA;
+  return TIM_OK;
+}
+
+// ----------------------------------------------------------------- correct --
+tim_status check_cfg(const tim_correct_cfg* c) {
+  if (!c) return TIM_ERR_NULL;
+  if (c->tis != 0 && c->tis != 1) return TIM_ERR_VALUE;
+  if (c->tok_rs != 0 && c->tok_rs != 1) return TIM_ERR_VALUE;
+  if (c->seq_rs != TIM_SEQ_NONE && c->seq_rs != TIM_SEQ_K1 && c->seq_rs != TIM_SEQ_K3) return TIM_ERR_VALUE;
+  if (c->seq_agg != TIM_AGG_SUM && c->seq_agg != TIM_AGG_MEAN) return TIM_ERR_VALUE;
+  if (c->tis && (!(c->tis_cap > 0.0) || !std::isfinite(c->tis_cap) || !std::isfinite(c->log_tis_cap)))
+    return TIM_ERR_VALUE;
+  if (c->tok_rs && (std::isnan(c->log_tok_lo) || std::isnan(c->log_tok_hi) || c->log_tok_lo > c->log_tok_hi))
+    return TIM_ERR_VALUE;
+  if (c->seq_rs != TIM_SEQ_NONE && (!std::isfinite(c->tau_seq) || std::fabs(c->tau_seq) >= 1024.0))
+    return TIM_ERR_VALUE;
+  return TIM_OK;
+}
+
+CorrectDevCfg dev_cfg(const tim_correct_cfg* c) {
+  CorrectDevCfg d{};
+  d.tis = c->tis;
+  d.tok_rs = c->tok_rs;
+  d.seq_rs = c->seq_rs;
+  d.seq_agg = c->seq_agg;
+  d.tis_cap = c->tis_cap;
+  d.log_tis_cap = c->log_tis_cap;
+  d.log_lo = c->log_tok_lo;
+  d.log_hi = c->log_tok_hi;
+  d.tau_seq = c->tau_seq;
+  return d;
+}
+
+tim_status check_common(const float* num, const float* den, const int64_t* cu, int64_t n_seq, int64_t tok_begin,
+                        int64_t n_local, const uint8_t* resp) {
+  if (!cu) return TIM_ERR_NULL;
+  if (n_local > 0 && (!num || !den)) return TIM_ERR_NULL;
+  if (n_seq < 0 || n_seq >= (int64_t(1) << 40) || n_local < 0 || tok_begin < 0) return TIM_ERR_SHAPE;
+  if (n_local > 0 && n_seq == 0) return TIM_ERR_SHAPE;
+  if (!aligned(num, 16) || !aligned(den, 16) || (resp && !aligned(resp, 8))) return TIM_ERR_ALIGN;
+  return TIM_OK;
+}
+
+// ------------------------------------------------------------------ NCCL --
+typedef struct { char internal[128]; } nccl_uid;
+typedef void* nccl_comm_t;
+typedef int (*PFN_getUniqueId)(nccl_uid*);
+typedef int (*PFN_commInitRank)(nccl_comm_t*, int, nccl_uid, int);
+typedef int (*PFN_allGather)(const void*, void*, size_t, int, nccl_comm_t, cudaStream_t);
+typedef int (*PFN_commDestroy)(nccl_comm_t);
+struct NcclApi {
+  bool ok = false;
+  PFN_getUniqueId get_uid = nullptr;
+  PFN_commInitRank init_rank = nullptr;
+  PFN_allGather all_gather = nullptr;
+  PFN_commDestroy destroy = nullptr;
+};
+NcclApi* nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.get_uid = reinterpret_cast<PFN_getUniqueId>(dlsym(h, "ncclGetUniqueId"));
+    api.init_rank = reinterpret_cast<PFN_commInitRank>(dlsym(h, "ncclCommInitRank"));
+    api.all_gather = reinterpret_cast<PFN_allGather>(dlsym(h, "ncclAllGather"));
+    api.destroy = reinterpret_cast<PFN_commDestroy>(dlsym(h, "ncclCommDestroy"));
+    api.ok = api.get_uid && api.init_rank && api.all_gather && api.destroy;
+  });
+  return &api;
+}
+constexpr int kNcclInt8 = 0;
+
+}  // namespace
+
+struct tim_comm {
+  nccl_comm_t comm;
+  int nranks;
+  int rank;
+};
+
+// ======================================================================= C ABI ==
+extern "C" {
+
+const char* tim_status_string(tim_status s) {
+  switch (s) {
+    case TIM_OK: return "TIM_OK";
+    case TIM_ERR_NULL: return "TIM_ERR_NULL: a required pointer is NULL";
+    case TIM_ERR_SHAPE: return "TIM_ERR_SHAPE: size out of range or inconsistent";
+    case TIM_ERR_ALIGN: return "TIM_ERR_ALIGN: pointer / pitch violates the 16-byte (TMA) alignment";
+    case TIM_ERR_VALUE: return "TIM_ERR_VALUE: scalar parameter out of range";
+    case TIM_ERR_WORKSPACE: return "TIM_ERR_WORKSPACE: workspace too small";
+    case TIM_ERR_CUDA: return "TIM_ERR_CUDA: CUDA call failed";
+    case TIM_ERR_NCCL: return "TIM_ERR_NCCL: NCCL unavailable or failed";
+    case TIM_ERR_UNSUPPORTED: return "TIM_ERR_UNSUPPORTED: requires an sm_100 (B200) device";
+    case TIM_ERR_DATA: return "TIM_ERR_DATA: device-side data error (see first_bad_index)";
+  }
+  return "unknown tim_status";
+}
+
+int tim_abi_version(void) { return TIM_ABI_VERSION; }
+
+int32_t tim_logprob_vocab_slices(int32_t vocab) { return vocab < 1 ? 0 : vocab_slices(vocab); }
+
+size_t tim_logprob_workspace_bytes(int64_t n_tok, int32_t hidden, int32_t vocab) {
+  (void)hidden;
+  if (n_tok < 0 || vocab < 1) return 0;
+  return kWsHeaderBytes + static_cast<size_t>(vocab_slices(vocab)) * static_cast<size_t>(n_tok) * 16u;
+}
+
+tim_status tim_logprob(const void* hidden_bf16, int64_t ld_hidden, const void* weight_bf16, int32_t hidden,
+                       int32_t vocab, const int64_t* token_ids, int64_t n_tok, float temperature,
+                       const float* temperatures_or_null, float* logp_out, float* entropy_out_or_null,
+                       void* workspace, size_t workspace_bytes, tim_device_status* dstatus, void* stream) {
+  return logprob_impl(hidden_bf16, ld_hidden, weight_bf16, hidden, vocab, token_ids, n_tok, temperature,
+                      temperatures_or_null, logp_out, entropy_out_or_null, workspace, workspace_bytes, dstatus,
+                      stream, nullptr, 0);
+}
+
+tim_status tim_stats_finalize(tim_stats* h) {
+  if (!h) return TIM_ERR_NULL;
+  auto to_d = [](const int64_t* v) {
+    const __int128 x = (static_cast<__int128>(v[1]) << 64) | static_cast<__int128>(static_cast<uint64_t>(v[0]));
+    const bool neg = x < 0;
+    unsigned __int128 u = neg ? static_cast<unsigned __int128>(-x) : static_cast<unsigned __int128>(x);
+    const uint64_t hi = static_cast<uint64_t>(u >> 64);
+    double r;
+    if (hi == 0) {
+      r = static_cast<double>(static_cast<uint64_t>(u));  // RN (default rounding mode)
+    } else {
+      const int sh = 64 - __builtin_clzll(hi);
+      uint64_t top = static_cast<uint64_t>(u >> sh);
+      if ((u & ((static_cast<unsigned __int128>(1) << sh) - 1)) != 0) top |= 1u;
+      r = std::ldexp(static_cast<double>(top), sh);
+    }
+    return neg ? -r : r;
+  };
+  const double n = static_cast<double>(h->n_resp_tok);
+  const double sc = std::ldexp(1.0, -52);
+  h->mean_abs_delta = h->n_resp_tok ? (to_d(h->sum_abs_delta_fx) * sc) / n : 0.0;
+  h->mean_k1 = h->n_resp_tok ? (to_d(h->sum_k1_fx) * sc) / n : 0.0;
+  h->mean_k3 = h->n_resp_tok ? (to_d(h->sum_k3_fx) * sc) / n : 0.0;
+  return TIM_OK;
+}
+
+size_t tim_correct_partial_bytes(int64_t n_seq) {
+  if (n_seq < 0) return 0;
+  return sizeof(tim_partial_header) + static_cast<size_t>(n_seq) * sizeof(tim_seq_partial);
+}
+
+size_t tim_correct_workspace_bytes(int64_t n_tok_local, int64_t n_seq, int32_t nranks) {
+  (void)n_tok_local;
+  if (n_seq < 0 || nranks < 1) return 0;
+  const size_t b = (tim_correct_partial_bytes(n_seq) + 255) & ~size_t(255);
+  return b * (1 + (nranks > 1 ? static_cast<size_t>(nranks) : 0));
+}
+
+tim_status tim_correct_local(const float* num, const float* den, const int64_t* cu, int64_t n_seq,
+                             int64_t tok_begin, int64_t n_local, const uint8_t* resp, const tim_correct_cfg* cfg,
+                             float* tis_w, uint8_t* tok_keep, float* coeff, void* partial_out,
+                             tim_device_status* dstatus, void* stream) {
+  tim_status st = check_common(num, den, cu, n_seq, tok_begin, n_local, resp);
+  if (st != TIM_OK) return st;
+  if ((st = check_cfg(cfg)) != TIM_OK) return st;
+  const bool any_out = tis_w || tok_keep || coeff;
+  if (!partial_out) return TIM_ERR_NULL;
+  if (any_out && !(tis_w && tok_keep && coeff)) return TIM_ERR_NULL;
+  if (any_out && (!aligned(tis_w, 16) || !aligned(coeff, 16) || !aligned(tok_keep, 8))) return TIM_ERR_ALIGN;
+  if (!aligned(partial_out, 16)) return TIM_ERR_ALIGN;
+  DevInfo* dev = nullptr;
+  if ((st = device_info(&dev)) != TIM_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(partial_out, 0, tim_correct_partial_bytes(n_seq), s) != cudaSuccess) return TIM_ERR_CUDA;
+  if (n_local == 0) return TIM_OK;
+  LocalParams p{};
+  p.num = num;
+  p.den = den;
+  p.cu = cu;
+  p.n_seq = n_seq;
+  p.tok_begin = tok_begin;
+  p.n = n_local;
+  p.resp = resp;
+  p.tis_w = tis_w;
+  p.tok_keep = tok_keep;
+  p.coeff = coeff;
+  p.hdr = static_cast<tim_partial_header*>(partial_out);
+  p.seqp = reinterpret_cast<tim_seq_partial*>(static_cast<uint8_t*>(partial_out) + sizeof(tim_partial_header));
+  p.cfg = dev_cfg(cfg);
+  p.dstatus = dstatus;
+  return launch_correct_local(p, dev->num_sms, s) == cudaSuccess ? TIM_OK : TIM_ERR_CUDA;
+}
+
+tim_status tim_correct_finish(const void* gathered, int32_t nranks, const int64_t* cu, int64_t n_seq,
+                              int64_t tok_begin, int64_t n_local, const tim_correct_cfg* cfg, float* coeff,
+                              uint8_t* seq_keep, double* seq_score, tim_stats* stats, void* stream) {
+  if (!gathered || !cu) return TIM_ERR_NULL;
+  if (nranks < 1 || n_seq < 0 || n_local < 0 || tok_begin < 0) return TIM_ERR_SHAPE;
+  tim_status st = check_cfg(cfg);
+  if (st != TIM_OK) return st;
+  if (cfg->seq_rs != TIM_SEQ_NONE && n_local > 0 && !coeff) return TIM_ERR_NULL;
+  if (!aligned(gathered, 16)) return TIM_ERR_ALIGN;
+  DevInfo* dev = nullptr;
+  if ((st = device_info(&dev)) != TIM_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  FinishParams f{};
+  f.gathered = static_cast<const uint8_t*>(gathered);
+  f.block_bytes = static_cast<int64_t>(tim_correct_partial_bytes(n_seq));
+  f.nranks = nranks;
+  f.n_seq = n_seq;
+  f.cfg = dev_cfg(cfg);
+  f.seq_keep = seq_keep;
+  f.seq_score = seq_score;
+  f.stats = stats;
+  if (launch_correct_finish(f, s) != cudaSuccess) return TIM_ERR_CUDA;
+  if (cfg->seq_rs != TIM_SEQ_NONE && n_local > 0 && n_seq > 0) {
+    if (!seq_keep) return TIM_ERR_NULL;
+    ZeroParams z{};
+    z.cu = cu;
+    z.n_seq = n_seq;
+    z.tok_begin = tok_begin;
+    z.n = n_local;
+    z.seq_keep = seq_keep;
+    z.coeff = coeff;
+    if (launch_correct_zero(z, s) != cudaSuccess) return TIM_ERR_CUDA;
+  }
+  return TIM_OK;
+}
+
+static tim_status correct_impl(const float* num, const float* den, const int64_t* cu, int64_t n_seq,
+                               int64_t tok_begin, int64_t n_local, const uint8_t* resp, const tim_correct_cfg* cfg,
+                               tim_comm* comm, float* tis_w, uint8_t* tok_keep, uint8_t* seq_keep, float* coeff,
+                               double* seq_score, tim_stats* stats, void* ws, size_t ws_bytes,
+                               tim_device_status* dstatus, void* stream) {
+  tim_status st = check_common(num, den, cu, n_seq, tok_begin, n_local, resp);
+  if (st != TIM_OK) return st;
+  if ((st = check_cfg(cfg)) != TIM_OK) return st;
+  const int nranks = comm ? comm->nranks : 1;
+  if (!ws) return TIM_ERR_NULL;
+  if (!aligned(ws, 256)) return TIM_ERR_ALIGN;
+  if (ws_bytes < tim_correct_workspace_bytes(n_local, n_seq, nranks)) return TIM_ERR_WORKSPACE;
+  if (seq_keep == nullptr && cfg->seq_rs != TIM_SEQ_NONE && tis_w) return TIM_ERR_NULL;
+  uint8_t* local = static_cast<uint8_t*>(ws);
+  const size_t blk = (tim_correct_partial_bytes(n_seq) + 255) & ~size_t(255);
+  if ((st = tim_correct_local(num, den, cu, n_seq, tok_begin, n_local, resp, cfg, tis_w, tok_keep, coeff, local,
+                              dstatus, stream)) != TIM_OK)
+    return st;
+  const void* gathered = local;
+  if (nranks > 1) {
+    NcclApi* api = nccl();
+    if (!api->ok) return TIM_ERR_NCCL;
+    uint8_t* g = local + blk;
+    // the gathered buffer is [nranks][partial_bytes] with no padding between blocks
+    if (api->all_gather(local, g, tim_correct_partial_bytes(n_seq), kNcclInt8, comm->comm,
+                        reinterpret_cast<cudaStream_t>(stream)) != 0)
+      return TIM_ERR_NCCL;
+    gathered = g;
+  }
+  return tim_correct_finish(gathered, nranks, cu, n_seq, tok_begin, n_local, cfg, coeff, seq_keep, seq_score, stats,
+                            stream);
+}
+
+tim_status tim_mismatch_stats(const float* num, const float* den, const int64_t* cu, int64_t n_seq,
+                              int64_t tok_begin, int64_t n_local, const uint8_t* resp, tim_comm* comm,
+                              tim_stats* stats_dev, void* ws, size_t ws_bytes, tim_device_status* dstatus,
+                              void* stream) {
+  if (!stats_dev) return TIM_ERR_NULL;
+  tim_correct_cfg cfg{};
+  cfg.tis = 0;
+  cfg.tok_rs = 0;
+  cfg.seq_rs = TIM_SEQ_NONE;
+  cfg.seq_agg = TIM_AGG_SUM;
+  return correct_impl(num, den, cu, n_seq, tok_begin, n_local, resp, &cfg, comm, nullptr, nullptr, nullptr, nullptr,
+                      nullptr, stats_dev, ws, ws_bytes, dstatus, stream);
+}
+
+tim_status tim_correct(const float* num, const float* den, const int64_t* cu, int64_t n_seq, int64_t tok_begin,
+                       int64_t n_local, const uint8_t* resp, const tim_correct_cfg* cfg, tim_comm* comm,
+                       float* tis_w, uint8_t* tok_keep, uint8_t* seq_keep, float* coeff, double* seq_score,
+                       tim_stats* stats_dev, void* ws, size_t ws_bytes, tim_device_status* dstatus,
+                       void* stream) {
+  if (!tis_w || !tok_keep || !coeff || !seq_keep) return TIM_ERR_NULL;
+  return correct_impl(num, den, cu, n_seq, tok_begin, n_local, resp, cfg, comm, tis_w, tok_keep, seq_keep, coeff,
+                      seq_score, stats_dev, ws, ws_bytes, dstatus, stream);
+}
+
+tim_status tim_comm_unique_id(void* out) {
+  if (!out) return TIM_ERR_NULL;
+  NcclApi* api = nccl();
+  if (!api->ok) return TIM_ERR_NCCL;
+  nccl_uid id;
+  if (api->get_uid(&id) != 0) return TIM_ERR_NCCL;
+  std::memcpy(out, &id, sizeof(id));
+  return TIM_OK;
+}
+
+tim_status tim_comm_init(const void* uid, int32_t nranks, int32_t rank, tim_comm** out) {
+  if (!uid || !out) return TIM_ERR_NULL;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return TIM_ERR_SHAPE;
+  NcclApi* api = nccl();
+  if (!api->ok) return TIM_ERR_NCCL;
+  nccl_uid id;
+  std::memcpy(&id, uid, sizeof(id));
+  nccl_comm_t c = nullptr;
+  if (api->init_rank(&c, nranks, id, rank) != 0) return TIM_ERR_NCCL;
+  tim_comm* t = new tim_comm{c, nranks, rank};
+  *out = t;
+  return TIM_OK;
+}
+
+tim_status tim_comm_destroy(tim_comm* comm) {
+  if (!comm) return TIM_ERR_NULL;
+  NcclApi* api = nccl();
+  if (api->ok && comm->comm) api->destroy(comm->comm);
+  delete comm;
+  return TIM_OK;
+}
+
+// ---------------------------------------------------------------- debug ABI --
+tim_status tim_debug_logprob_logits(const void* hidden_bf16, int64_t ld_hidden, const void* weight_bf16,
+                                    int32_t hidden, int32_t vocab, const int64_t* token_ids, int64_t n_tok,
+                                    float* logits_out, int64_t ld_logits, float* logp_out, float* entropy_out,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
+  if (!logits_out) return TIM_ERR_NULL;
+  if (ld_logits < vocab) return TIM_ERR_SHAPE;
+  return logprob_impl(hidden_bf16, ld_hidden, weight_bf16, hidden, vocab, token_ids, n_tok, 1.0f, nullptr, logp_out,
+                      entropy_out, workspace, workspace_bytes, nullptr, stream, logits_out, ld_logits);
+}
+
+tim_status tim_debug_set_kernel(int32_t use_pair, int32_t max_ctas_or_clusters) {
+  if (use_pair != 0 && use_pair != 1) return TIM_ERR_VALUE;
+  if (max_ctas_or_clusters < 0) return TIM_ERR_VALUE;
+  g_use_pair = use_pair;
+  g_max_clusters = max_ctas_or_clusters;
+  return TIM_OK;
+}
+
+}  // extern "C"

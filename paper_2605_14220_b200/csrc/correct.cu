@@ -1,0 +1,505 @@
+// correct.cu -- mismatch statistics and TIS / RS corrections.
+//
+// Real-number semantics from PAPER.md: delta_t (§2), r_corr = e^delta (§4.2),
+// w = min(r_corr, tau_tok) (L_TIS P:497-507), K1 = -log r, K3 = (r-1) - log r (§4.1),
+// S_seq = sum_t K(q_t) and 1[S_seq <= tau_seq] (L_RS P:509-547, App. A.4).
+//
+// Integer outputs (masks, counts, sequence decisions) are bit-exact by construction through
+// the decision-path arithmetic contract: every fp64 op is an
+// explicit round-to-nearest intrinsic (__dadd_rn / __dsub_rn / __dmul_rn: never contracted to
+// FMA), no transcendental from libm sits on the decision path, the per-token K values are turned
+// into exact 2^-52 fixed point and all sums are int128 integer sums -- exact, so independent of
+// the reduction order, of atomics order, of sharding and of the GPU count.
+//
+// Layout: structure-of-arrays fp32 / u8 token vectors, one warp owns 256 consecutive tokens
+// (8 per lane, 32-B vector loads), so every load and store is fully coalesced.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstdint>
+
+#include "tim_internal.h"
+
+namespace tim {
+
+// RN(1/n!), n = 0..23 (binary64), and the Cody-Waite split of ln 2 (fdlibm ln2_hi / ln2_lo).
+__constant__ double kInvFact[24] = {
+    0x1.0000000000000p+0,  0x1.0000000000000p+0,  0x1.0000000000000p-1,  0x1.5555555555555p-3,
+    0x1.5555555555555p-5,  0x1.1111111111111p-7,  0x1.6c16c16c16c17p-10, 0x1.a01a01a01a01ap-13,
+    0x1.a01a01a01a01ap-16, 0x1.71de3a556c734p-19, 0x1.27e4fb7789f5cp-22, 0x1.ae64567f544e4p-26,
+    0x1.1eed8eff8d898p-29, 0x1.6124613a86d09p-33, 0x1.93974a8c07c9dp-37, 0x1.ae7f3e733b81fp-41,
+    0x1.ae7f3e733b81fp-45, 0x1.952c77030ad4ap-49, 0x1.6827863b97d97p-53, 0x1.2f49b46814157p-57,
+    0x1.e542ba4020225p-62, 0x1.71b8ef6dcf572p-66, 0x1.0ce396db7f853p-70, 0x1.761b41316381ap-75};
+constexpr double kLog2e = 0x1.71547652b82fep+0;
+constexpr double kLn2Hi = 0x1.62e42fee00000p-1;
+constexpr double kLn2Lo = 0x1.a39ef35793c76p-33;
+constexpr double kTwo52 = 0x1p52;
+constexpr long long kSatX = 1ll << 62;
+
+// e^d: k = rint(d log2 e), r = (d - k ln2_hi) - k ln2_lo, degree-13 Taylor (Horner), * 2^k.
+__device__ __forceinline__ double exp_c(double d) {
+  if (d > 709.0) return CUDART_INF;
+  if (d < -700.0) return 0.0;
+  const double k = rint(__dmul_rn(d, kLog2e));
+  const double r = __dsub_rn(__dsub_rn(d, __dmul_rn(k, kLn2Hi)), __dmul_rn(k, kLn2Lo));
+  double p = kInvFact[13];
+#pragma unroll
+  for (int n = 12; n >= 0; --n) p = __dadd_rn(__dmul_rn(p, r), kInvFact[n]);
+  const long long ki = static_cast<long long>(k);  // in [-1010, 1023]: 2^k is a normal double
+  return __dmul_rn(p, __longlong_as_double((ki + 1023) << 52));
+}
+
+// K3 = e^d - 1 - d: Horner series of (e^d - 1 - d) / d^2 for |d| <= 1, else via exp_c.
+__device__ __forceinline__ double k3_c(double d) {
+  if (fabs(d) <= 1.0) {
+    double P = kInvFact[23];
+#pragma unroll
+    for (int n = 22; n >= 2; --n) P = __dadd_rn(__dmul_rn(P, d), kInvFact[n]);
+    return __dmul_rn(__dmul_rn(d, d), P);
+  }
+  return __dsub_rn(__dsub_rn(exp_c(d), 1.0), d);
+}
+
+// X = rint(K 2^52); |K| > 2^10 or NaN/inf saturates to sign(K) 2^62.
+__device__ __forceinline__ long long fixed_point(double K, bool& sat) {
+  if (!(fabs(K) <= 1024.0)) {
+    sat = true;
+    return signbit(K) ? -kSatX : kSatX;
+  }
+  sat = false;
+  return __double2ll_rn(__dmul_rn(K, kTwo52));
+}
+
+__device__ __forceinline__ void atomic_add_i128(int64_t* p, __int128 v) {
+  const unsigned long long lo = static_cast<unsigned long long>(v);
+  unsigned long long hi = static_cast<unsigned long long>(v >> 64);
+  if (lo != 0) {
+    const unsigned long long old = atomicAdd(reinterpret_cast<unsigned long long*>(p), lo);
+    if (old + lo < old) hi += 1;  // carry out of the low word
+  }
+  if (hi != 0) atomicAdd(reinterpret_cast<unsigned long long*>(p + 1), hi);
+}
+
+__device__ __forceinline__ __int128 shfl_down_i128(__int128 v, int off) {
+  long long lo = static_cast<long long>(static_cast<unsigned long long>(v));
+  long long hi = static_cast<long long>(v >> 64);
+  lo = __shfl_down_sync(0xffffffffu, lo, off);
+  hi = __shfl_down_sync(0xffffffffu, hi, off);
+  return (static_cast<__int128>(hi) << 64) | static_cast<__int128>(static_cast<unsigned long long>(lo));
+}
+__device__ __forceinline__ __int128 warp_sum_i128(__int128 v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += shfl_down_i128(v, off);
+  return v;
+}
+__device__ __forceinline__ long long warp_sum_i64(long long v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+  return v;
+}
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long o = __shfl_down_sync(0xffffffffu, v, off);
+    v = o > v ? o : v;
+  }
+  return v;
+}
+
+struct SeqAcc {
+  long long sid;  // sequence id (LLONG_MAX: none)
+  __int128 x;
+  long long t, nsat;
+};
+
+__device__ __forceinline__ void flush_seq(tim_seq_partial* seqp, const SeqAcc& a) {
+  if (a.t == 0 && a.x == 0 && a.nsat == 0) return;
+  tim_seq_partial* d = seqp + a.sid;
+  atomic_add_i128(&d->x_lo, a.x);
+  if (a.t) atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_tok), static_cast<unsigned long long>(a.t));
+  if (a.nsat) atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_sat), static_cast<unsigned long long>(a.nsat));
+}
+
+// sequence containing global token g: last s with cu[s] <= g
+__device__ __forceinline__ long long seq_of(const int64_t* cu, long long n_seq, long long g) {
+  long long lo = 0, hi = n_seq;  // invariant cu[lo] <= g (cu[0] == 0), answer in [lo, hi)
+  while (hi - lo > 1) {
+    const long long mid = (lo + hi) >> 1;
+    if (__ldg(cu + mid) <= g) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+constexpr int kTpl = 8;                 // tokens per lane
+constexpr int kWarpTok = 32 * kTpl;     // tokens per warp chunk
+constexpr int kLocalThreads = 256;
+
+template <bool kOut, bool kSeq>
+__global__ void __launch_bounds__(kLocalThreads) correct_local_kernel(LocalParams p) {
+  const int lane = threadIdx.x & 31;
+  const long long warp_g = (static_cast<long long>(blockIdx.x) * kLocalThreads + threadIdx.x) >> 5;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * kLocalThreads) >> 5;
+  const long long n_chunks = (p.n + kWarpTok - 1) / kWarpTok;
+  const CorrectDevCfg cfg = p.cfg;
+
+  long long c_resp = 0, c_trunc = 0, c_rej = 0, c_sat = 0;
+  __int128 s_abs = 0, s_k1 = 0, s_k3 = 0;
+  unsigned long long maxbits = 0;
+  unsigned long long bad_inv = 0;
+
+  for (long long ch = warp_g; ch < n_chunks; ch += nwarps) {
+    const long long i0 = ch * kWarpTok + lane * kTpl;
+    float num[kTpl], den[kTpl];
+    uint8_t rs[kTpl];
+    const bool full = i0 + kTpl <= p.n;
+    if (full) {
+      const float4* pn = reinterpret_cast<const float4*>(p.num + i0);
+      const float4* pd = reinterpret_cast<const float4*>(p.den + i0);
+      const float4 n0 = __ldg(pn), n1 = __ldg(pn + 1), d0 = __ldg(pd), d1 = __ldg(pd + 1);
+      num[0] = n0.x; num[1] = n0.y; num[2] = n0.z; num[3] = n0.w;
+      num[4] = n1.x; num[5] = n1.y; num[6] = n1.z; num[7] = n1.w;
+      den[0] = d0.x; den[1] = d0.y; den[2] = d0.z; den[3] = d0.w;
+      den[4] = d1.x; den[5] = d1.y; den[6] = d1.z; den[7] = d1.w;
+      if (p.resp) {
+        const uint2 m = __ldg(reinterpret_cast<const uint2*>(p.resp + i0));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) rs[k] = (m.x >> (8 * k)) & 0xff;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) rs[4 + k] = (m.y >> (8 * k)) & 0xff;
+      } else {
+#pragma unroll
+        for (int k = 0; k < kTpl; ++k) rs[k] = 1;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kTpl; ++k) {
+        const long long i = i0 + k;
+        num[k] = i < p.n ? p.num[i] : 0.f;
+        den[k] = i < p.n ? p.den[i] : 0.f;
+        rs[k] = i < p.n ? (p.resp ? p.resp[i] : 1) : 0;
+      }
+    }
+
+    SeqAcc acc;
+    acc.sid = LLONG_MAX;
+    acc.x = 0;
+    acc.t = 0;
+    acc.nsat = 0;
+    long long next_b = 0;
+    if (kSeq && i0 < p.n) {
+      acc.sid = seq_of(p.cu, p.n_seq, p.tok_begin + i0);
+      next_b = __ldg(p.cu + acc.sid + 1);
+    }
+
+    float w_out[kTpl], c_out[kTpl];
+    uint8_t k_out[kTpl];
+#pragma unroll
+    for (int k = 0; k < kTpl; ++k) {
+      const long long i = i0 + k;
+      w_out[k] = 1.f;
+      c_out[k] = 0.f;
+      k_out[k] = 1;
+      if (i >= p.n) continue;
+      const long long g = p.tok_begin + i;
+      const double d = __dsub_rn(static_cast<double>(num[k]), static_cast<double>(den[k]));
+      if (!isfinite(d)) {  // C.3.2 data error: excluded from every sum, outputs NaN / 0
+        const unsigned long long b = kBadSentinel - static_cast<unsigned long long>(g);
+        bad_inv = b > bad_inv ? b : bad_inv;
+        w_out[k] = CUDART_NAN_F;
+        k_out[k] = 0;
+        continue;
+      }
+      const bool resp = rs[k] != 0;
+      const bool trunc = cfg.tis && d > cfg.log_tis_cap;
+      if (cfg.tis) {
+        const double w = trunc ? cfg.tis_cap : fmin(exp_c(d), cfg.tis_cap);
+        w_out[k] = __double2float_rn(w);
+      }
+      const bool keep = cfg.tok_rs ? (cfg.log_lo <= d && d <= cfg.log_hi) : true;
+      k_out[k] = keep ? 1 : 0;
+      c_out[k] = (resp && keep) ? w_out[k] : 0.f;
+
+      bool sat_abs, sat1, sat3;
+      const long long x1 = fixed_point(-d, sat1);
+      const double k3 = k3_c(d);
+      const long long x3 = fixed_point(k3, sat3);
+      if (resp) {
+        const long long xa = fixed_point(fabs(d), sat_abs);
+        c_resp += 1;
+        c_trunc += trunc ? 1 : 0;
+        c_rej += keep ? 0 : 1;
+        s_abs += xa;
+        s_k1 += x1;
+        s_k3 += x3;
+        const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(fabs(d)));
+        maxbits = bits > maxbits ? bits : maxbits;
+      }
+      if (kSeq) {
+        while (g >= next_b) {  // crossed into a later sequence (skips empty ones)
+          flush_seq(p.seqp, acc);
+          acc.x = 0;
+          acc.t = 0;
+          acc.nsat = 0;
+          acc.sid += 1;
+          next_b = __ldg(p.cu + acc.sid + 1);
+        }
+        if (resp && keep) {
+          const bool satq = cfg.seq_rs == TIM_SEQ_K1 ? sat1 : sat3;
+          acc.x += cfg.seq_rs == TIM_SEQ_K1 ? x1 : x3;
+          acc.t += 1;
+          acc.nsat += satq ? 1 : 0;
+          c_sat += satq ? 1 : 0;
+        }
+      }
+    }
+
+    if (kOut) {
+      if (full) {
+        float4* pw = reinterpret_cast<float4*>(p.tis_w + i0);
+        float4* pc = reinterpret_cast<float4*>(p.coeff + i0);
+        pw[0] = make_float4(w_out[0], w_out[1], w_out[2], w_out[3]);
+        pw[1] = make_float4(w_out[4], w_out[5], w_out[6], w_out[7]);
+        pc[0] = make_float4(c_out[0], c_out[1], c_out[2], c_out[3]);
+        pc[1] = make_float4(c_out[4], c_out[5], c_out[6], c_out[7]);
+        uint2 kk;
+        kk.x = k_out[0] | (k_out[1] << 8) | (k_out[2] << 16) | (static_cast<uint32_t>(k_out[3]) << 24);
+        kk.y = k_out[4] | (k_out[5] << 8) | (k_out[6] << 16) | (static_cast<uint32_t>(k_out[7]) << 24);
+        *reinterpret_cast<uint2*>(p.tok_keep + i0) = kk;
+      } else {
+#pragma unroll
+        for (int k = 0; k < kTpl; ++k) {
+          const long long i = i0 + k;
+          if (i < p.n) {
+            p.tis_w[i] = w_out[k];
+            p.coeff[i] = c_out[k];
+            p.tok_keep[i] = k_out[k];
+          }
+        }
+      }
+    }
+
+    if (kSeq) {
+      // segmented warp reduction of the open segments (sequence ids are non-decreasing in lane order)
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const long long osid = __shfl_down_sync(0xffffffffu, acc.sid, off);
+        const __int128 ox = shfl_down_i128(acc.x, off);
+        const long long ot = __shfl_down_sync(0xffffffffu, acc.t, off);
+        const long long on = __shfl_down_sync(0xffffffffu, acc.nsat, off);
+        if (lane + off < 32 && osid == acc.sid) {
+          acc.x += ox;
+          acc.t += ot;
+          acc.nsat += on;
+        }
+      }
+      // note: lane l now holds the sum of lanes [l, l+2^k) with the same id, so the head of each
+      // run (first lane of that id) holds the whole run because runs are contiguous.
+      const long long prev_sid = __shfl_up_sync(0xffffffffu, acc.sid, 1);
+      const bool head = lane == 0 || prev_sid != acc.sid;
+      if (head && acc.sid != LLONG_MAX) flush_seq(p.seqp, acc);
+    }
+  }
+
+  // block reduction of the global statistics, then one set of integer atomics per block
+  __shared__ long long sh_cnt[4][kLocalThreads / 32];
+  __shared__ long long sh_sum[6][kLocalThreads / 32];
+  __shared__ unsigned long long sh_max[kLocalThreads / 32], sh_bad[kLocalThreads / 32];
+  const int w = threadIdx.x >> 5;
+  c_resp = warp_sum_i64(c_resp);
+  c_trunc = warp_sum_i64(c_trunc);
+  c_rej = warp_sum_i64(c_rej);
+  c_sat = warp_sum_i64(c_sat);
+  s_abs = warp_sum_i128(s_abs);
+  s_k1 = warp_sum_i128(s_k1);
+  s_k3 = warp_sum_i128(s_k3);
+  maxbits = warp_max_u64(maxbits);
+  bad_inv = warp_max_u64(bad_inv);
+  if (lane == 0) {
+    sh_cnt[0][w] = c_resp;
+    sh_cnt[1][w] = c_trunc;
+    sh_cnt[2][w] = c_rej;
+    sh_cnt[3][w] = c_sat;
+    sh_sum[0][w] = static_cast<long long>(static_cast<unsigned long long>(s_abs));
+    sh_sum[1][w] = static_cast<long long>(s_abs >> 64);
+    sh_sum[2][w] = static_cast<long long>(static_cast<unsigned long long>(s_k1));
+    sh_sum[3][w] = static_cast<long long>(s_k1 >> 64);
+    sh_sum[4][w] = static_cast<long long>(static_cast<unsigned long long>(s_k3));
+    sh_sum[5][w] = static_cast<long long>(s_k3 >> 64);
+    sh_max[w] = maxbits;
+    sh_bad[w] = bad_inv;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long cnt[4] = {0, 0, 0, 0};
+    __int128 sums[3] = {0, 0, 0};
+    unsigned long long mx = 0, bd = 0;
+    for (int i = 0; i < kLocalThreads / 32; ++i) {
+      for (int k = 0; k < 4; ++k) cnt[k] += sh_cnt[k][i];
+      for (int k = 0; k < 3; ++k)
+        sums[k] += (static_cast<__int128>(sh_sum[2 * k + 1][i]) << 64) |
+                   static_cast<__int128>(static_cast<unsigned long long>(sh_sum[2 * k][i]));
+      mx = sh_max[i] > mx ? sh_max[i] : mx;
+      bd = sh_bad[i] > bd ? sh_bad[i] : bd;
+    }
+    tim_partial_header* h = p.hdr;
+    if (blockIdx.x == 0)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&h->n_tok), static_cast<unsigned long long>(p.n));
+    if (cnt[0]) atomicAdd(reinterpret_cast<unsigned long long*>(&h->n_resp_tok), static_cast<unsigned long long>(cnt[0]));
+    if (cnt[1]) atomicAdd(reinterpret_cast<unsigned long long*>(&h->n_truncated), static_cast<unsigned long long>(cnt[1]));
+    if (cnt[2]) atomicAdd(reinterpret_cast<unsigned long long*>(&h->n_tok_rejected), static_cast<unsigned long long>(cnt[2]));
+    if (cnt[3]) atomicAdd(reinterpret_cast<unsigned long long*>(&h->n_saturated), static_cast<unsigned long long>(cnt[3]));
+    atomic_add_i128(h->sum_abs_delta, sums[0]);
+    atomic_add_i128(h->sum_k1, sums[1]);
+    atomic_add_i128(h->sum_k3, sums[2]);
+    if (mx) atomicMax(reinterpret_cast<unsigned long long*>(&h->max_abs_delta_bits), mx);
+    if (bd) atomicMax(reinterpret_cast<unsigned long long*>(&h->reserved[0]), bd);
+  }
+  // status commit by the last block (ticket in hdr->reserved[1], bad index in reserved[0])
+  commit_status_last_block(reinterpret_cast<WsHeader*>(&p.hdr->reserved[0]), p.dstatus);
+}
+
+// exact int128 -> double, round to nearest even
+__device__ __forceinline__ double i128_to_double(__int128 x) {
+  const bool neg = x < 0;
+  unsigned __int128 u = neg ? static_cast<unsigned __int128>(-x) : static_cast<unsigned __int128>(x);
+  const unsigned long long hi = static_cast<unsigned long long>(u >> 64);
+  double r;
+  if (hi == 0) {
+    r = __ull2double_rn(static_cast<unsigned long long>(u));
+  } else {
+    const int sh = 64 - __clzll(hi);  // bits above the low 64
+    unsigned long long top = static_cast<unsigned long long>(u >> sh);
+    const unsigned __int128 rem = u & ((static_cast<unsigned __int128>(1) << sh) - 1);
+    if (rem != 0) top |= 1ull;  // sticky: bit 0 lies 11 bits below the rounding position
+    r = __dmul_rn(__ull2double_rn(top), __longlong_as_double(static_cast<long long>(sh + 1023) << 52));
+  }
+  return neg ? -r : r;
+}
+
+__device__ __forceinline__ __int128 ld_i128(const int64_t* p) {
+  return (static_cast<__int128>(p[1]) << 64) | static_cast<__int128>(static_cast<unsigned long long>(p[0]));
+}
+
+// floor(tau * 2^52 * T) exactly: tau = mant * 2^e (frexp), M = mant * 2^53 an integer,
+// tau 2^52 T = M T 2^(e-1).  |tau| < 2^10 => e <= 11, M T < 2^84: fits int128.
+__device__ __forceinline__ __int128 seq_threshold(double tau, long long T) {
+  int e;
+  const double mant = frexp(tau, &e);
+  const long long M = static_cast<long long>(__dmul_rn(mant, 0x1p53));
+  const __int128 MT = static_cast<__int128>(M) * T;
+  const int sh = e - 1;
+  return sh >= 0 ? (MT << sh) : (MT >> (-sh));  // arithmetic shift = floor
+}
+
+constexpr int kFinishThreads = 1024;
+
+__global__ void __launch_bounds__(kFinishThreads) correct_finish_kernel(FinishParams p) {
+  const CorrectDevCfg cfg = p.cfg;
+  __shared__ int sh_rej[kFinishThreads / 32];
+  int rej = 0;
+  for (long long s = threadIdx.x; s < p.n_seq; s += blockDim.x) {
+    __int128 X = 0;
+    long long T = 0, nsat = 0;
+    for (int r = 0; r < p.nranks; ++r) {  // fixed rank order (exact anyway)
+      const tim_seq_partial* sp = reinterpret_cast<const tim_seq_partial*>(
+          p.gathered + r * p.block_bytes + sizeof(tim_partial_header)) + s;
+      X += ld_i128(&sp->x_lo);
+      T += sp->n_tok;
+      nsat += sp->n_sat;
+    }
+    uint8_t keep = 1;
+    double score = 0.0;
+    if (cfg.seq_rs != TIM_SEQ_NONE) {
+      score = __dmul_rn(i128_to_double(X), 0x1p-52);
+      if (cfg.seq_agg == TIM_AGG_MEAN) score = T > 0 ? __ddiv_rn(score, static_cast<double>(T)) : 0.0;
+      if (T == 0) keep = 1;
+      else if (nsat > 0) keep = 0;
+      else keep = X <= seq_threshold(cfg.tau_seq, cfg.seq_agg == TIM_AGG_MEAN ? T : 1) ? 1 : 0;
+    }
+    rej += keep ? 0 : 1;
+    if (p.seq_keep) p.seq_keep[s] = keep;
+    if (p.seq_score) p.seq_score[s] = score;
+  }
+  for (int off = 16; off > 0; off >>= 1) rej += __shfl_down_sync(0xffffffffu, rej, off);
+  if ((threadIdx.x & 31) == 0) sh_rej[threadIdx.x >> 5] = rej;
+  __syncthreads();
+  if (threadIdx.x == 0 && p.stats) {
+    long long n_rej = 0;
+    for (int i = 0; i < kFinishThreads / 32; ++i) n_rej += sh_rej[i];
+    long long cnt[5] = {0, 0, 0, 0, 0};
+    __int128 sums[3] = {0, 0, 0};
+    unsigned long long mx = 0;
+    for (int r = 0; r < p.nranks; ++r) {
+      const tim_partial_header* h = reinterpret_cast<const tim_partial_header*>(p.gathered + r * p.block_bytes);
+      cnt[0] += h->n_tok;
+      cnt[1] += h->n_resp_tok;
+      cnt[2] += h->n_truncated;
+      cnt[3] += h->n_tok_rejected;
+      cnt[4] += h->n_saturated;
+      sums[0] += ld_i128(h->sum_abs_delta);
+      sums[1] += ld_i128(h->sum_k1);
+      sums[2] += ld_i128(h->sum_k3);
+      mx = h->max_abs_delta_bits > mx ? h->max_abs_delta_bits : mx;
+    }
+    tim_stats* st = p.stats;
+    st->n_tok = cnt[0];
+    st->n_resp_tok = cnt[1];
+    st->n_seq = p.n_seq;
+    st->n_truncated = cnt[2];
+    st->n_tok_rejected = cnt[3];
+    st->n_seq_rejected = n_rej;
+    st->n_saturated = cnt[4];
+    st->sum_abs_delta_fx[0] = static_cast<int64_t>(static_cast<unsigned long long>(sums[0]));
+    st->sum_abs_delta_fx[1] = static_cast<int64_t>(sums[0] >> 64);
+    st->sum_k1_fx[0] = static_cast<int64_t>(static_cast<unsigned long long>(sums[1]));
+    st->sum_k1_fx[1] = static_cast<int64_t>(sums[1] >> 64);
+    st->sum_k3_fx[0] = static_cast<int64_t>(static_cast<unsigned long long>(sums[2]));
+    st->sum_k3_fx[1] = static_cast<int64_t>(sums[2] >> 64);
+    st->max_abs_delta = __longlong_as_double(static_cast<long long>(mx));
+    st->mean_abs_delta = 0.0;
+    st->mean_k1 = 0.0;
+    st->mean_k3 = 0.0;
+  }
+}
+
+// Zero the coefficient of this rank's tokens that belong to rejected sequences.
+__global__ void __launch_bounds__(256) correct_zero_kernel(ZeroParams p) {
+  const long long te = p.tok_begin + p.n;
+  for (long long s = blockIdx.x; s < p.n_seq; s += gridDim.x) {
+    if (p.seq_keep[s]) continue;
+    const long long c0 = p.cu[s], c1 = p.cu[s + 1], tb = p.tok_begin;
+    const long long a = c0 > tb ? c0 : tb;
+    const long long b = c1 < te ? c1 : te;
+    for (long long g = a + threadIdx.x; g < b; g += blockDim.x) p.coeff[g - p.tok_begin] = 0.f;
+  }
+}
+
+cudaError_t launch_correct_local(const LocalParams& p, int num_sms, cudaStream_t stream) {
+  const long long chunks = (p.n + kWarpTok - 1) / kWarpTok;
+  const long long warps_per_block = kLocalThreads / 32;
+  long long blocks = (chunks + warps_per_block - 1) / warps_per_block;
+  const long long cap = static_cast<long long>(num_sms) * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  const bool out = p.tis_w != nullptr;
+  const bool seq = p.cfg.seq_rs != TIM_SEQ_NONE;
+  if (out && seq) correct_local_kernel<true, true><<<blocks, kLocalThreads, 0, stream>>>(p);
+  else if (out) correct_local_kernel<true, false><<<blocks, kLocalThreads, 0, stream>>>(p);
+  else if (seq) correct_local_kernel<false, true><<<blocks, kLocalThreads, 0, stream>>>(p);
+  else correct_local_kernel<false, false><<<blocks, kLocalThreads, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_correct_finish(const FinishParams& p, cudaStream_t stream) {
+  correct_finish_kernel<<<1, kFinishThreads, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_correct_zero(const ZeroParams& p, cudaStream_t stream) {
+  long long blocks = p.n_seq < 4096 ? p.n_seq : 4096;
+  if (blocks < 1) return cudaSuccess;
+  correct_zero_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace tim

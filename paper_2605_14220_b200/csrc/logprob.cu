@@ -1,0 +1,335 @@
+// logprob.cu -- tim_logprob device code.
+//
+// a2  lm_head contraction z = H W^T on the 5th-gen tensor cores: tcgen05.mma kind::f16,
+//     bf16 x bf16 -> fp32 accumulators in TMEM (never rounded to bf16), operands staged in
+//     shared memory by TMA (128-byte swizzle), a CTA pair (cta_group::2) computes a 256-token x
+//     256-vocab tile; K ascending in steps of 16 from a zeroed accumulator.
+// a3  fused epilogue: each epilogue thread owns one token row (TMEM lane), reads 32 columns
+//     at a time with tcgen05.ld and keeps an online (max m, sum-exp s, sum p*(y-m) u, gathered
+//     y_a) in registers -- log2 domain, y = z * log2(e) / T.  Logits never reach HBM.
+// a4  fixed-order vocab-slice merge (merge kernel): slices 0..S_v-1 in order, fp64.
+//
+// Batch invariance (§3.1): a token row's arithmetic depends only on its
+// own H row, W and constants of (V, d): the vocab tile (256), the slice split S_v(V), the K
+// order and the MMA shape.  Which CTA, which row slot, how many rows, SMs or GPUs -- none
+// of these enter the arithmetic of a row.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstdint>
+
+#include "ptx.cuh"
+#include "tim_internal.h"
+
+namespace tim {
+
+constexpr int kBlockK = 64;        // K elements per pipeline stage (128 B rows -> SW128)
+constexpr int kUmmaK = 16;         // K per tcgen05.mma kind::f16
+constexpr int kCtaM = 128;         // token rows per CTA (= TMEM lanes)
+constexpr int kTileN = 256;        // vocab columns per tile (MMA N)
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr float kLog2eF = 1.44269504088896340736f;
+
+template <bool kPair>
+struct KCfg {
+  static constexpr int kBRows = kPair ? 128 : 256;  // W rows staged per CTA
+  static constexpr int kABytes = kCtaM * kBlockK * 2;
+  static constexpr int kBBytes = kBRows * kBlockK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = kPair ? 6 : 4;
+  static constexpr int kUnitM = kPair ? 2 * kCtaM : kCtaM;
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
+  static constexpr int kCtaGroup = kPair ? 2 : 1;
+};
+
+__device__ __forceinline__ float chunk_max32(const float (&y)[32]) {
+  float a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = fmaxf(y[i], y[i + 16]);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = fmaxf(a[i], a[i + 8]);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) a[i] = fmaxf(a[i], a[i + 4]);
+  return fmaxf(fmaxf(a[0], a[2]), fmaxf(a[1], a[3]));
+}
+
+// Online update of the row state with 32 consecutive columns (fixed order, fixed tree).
+template <bool kTail>
+__device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float c, int col0, int vocab, int64_t a,
+                                          float& m, float& s, float& u, float& ya) {
+  float y[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    y[i] = __uint_as_float(r[i]) * c;
+    if (kTail && col0 + i >= vocab) y[i] = -CUDART_INF_F;
+  }
+  const float cmax = chunk_max32(y);
+  const int64_t rel = a - col0;
+  if (static_cast<uint64_t>(rel) < 32u) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (rel == i) ya = y[i];
+  }
+  if (cmax > m) {
+    const float dm = m - cmax;  // -inf on the first chunk of a slice
+    const float sc = ex2_approx(dm);
+    u = (s > 0.f) ? sc * fmaf(s, dm, u) : 0.f;
+    s = s * sc;
+    m = cmax;
+  }
+  float s4[4] = {0.f, 0.f, 0.f, 0.f}, u4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    float t = y[i] - m;
+    if (kTail) t = fmaxf(t, -256.f);  // masked column: e = 0, e * t = 0 (no -inf * 0)
+    const float e = ex2_approx(t);
+    s4[i & 3] += e;
+    u4[i & 3] = fmaf(e, t, u4[i & 3]);
+  }
+  s += (s4[0] + s4[1]) + (s4[2] + s4[3]);
+  u += (u4[0] + u4[1]) + (u4[2] + u4[3]);
+}
+
+template <bool kPair, bool kDebug>
+__global__ void __launch_bounds__(kThreads, 1)
+    logprob_fwd_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constant__ CUtensorMap tmap_w,
+                       LogprobParams p) {
+  using C = KCfg<kPair>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + C::kStages * C::kABytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + C::kStages;
+  uint64_t* tfull = bars + 2 * C::kStages;
+  uint64_t* tempty = bars + 2 * C::kStages + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::kStages + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = kPair ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const uint32_t cid = kPair ? cluster_id_x() : blockIdx.x;
+  const uint32_t ncl = kPair ? ncluster_x() : gridDim.x;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(smem_u32(&tfull[a]), 1);
+      mbar_init(smem_u32(&tempty[a]), kPair ? 2 * kEpiWarps : kEpiWarps);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmap_h);
+    tma_prefetch(&tmap_w);
+  }
+  if (warp == 1) tmem_alloc<C::kCtaGroup>(smem_u32(tmem_slot), 512);
+  tc_fence_before();
+  if (kPair) cluster_sync(); else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int n_slices = p.n_slices;
+  const int n_units = p.n_mt * n_slices;
+  const int nkb = p.hidden / kBlockK;
+
+  if (warp == 0) {
+    // ===================== TMA producer (one thread per CTA) =====================
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (int u = cid; u < n_units; u += ncl) {
+        const int j = u / p.n_mt, mt = u % p.n_mt;
+        const int m0 = mt * C::kUnitM + rank * kCtaM;
+        const int t0 = (j * p.n_vt) / n_slices, t1 = ((j + 1) * p.n_vt) / n_slices;
+        for (int vt = t0; vt < t1; ++vt) {
+          const int n0 = vt * kTileN + rank * C::kBRows;
+          for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+            const uint32_t fb_local = smem_u32(&full[stage]);
+            const uint32_t a_dst = smem_u32(smem_a + stage * C::kABytes);
+            const uint32_t b_dst = smem_u32(smem_b + stage * C::kBBytes);
+            if (kPair) {
+              if (leader) mbar_arrive_expect_tx(fb_local, 2 * C::kStageBytes);
+              const uint32_t fb = mapa(fb_local, 0);
+              tma_load_2d_pair(a_dst, &tmap_h, fb, kb * kBlockK, m0);
+              tma_load_2d_pair(b_dst, &tmap_w, fb, kb * kBlockK, n0);
+            } else {
+              mbar_arrive_expect_tx(fb_local, C::kStageBytes);
+              tma_load_2d(a_dst, &tmap_h, fb_local, kb * kBlockK, m0);
+              tma_load_2d(b_dst, &tmap_w, fb_local, kb * kBlockK, n0);
+            }
+            if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (one thread of the leader CTA) =====================
+    if (leader && lane == 0) {
+      const uint32_t idesc = umma_idesc_bf16_f32(kPair ? 256 : 128, kTileN);
+      const uint16_t mask = kPair ? 0x3 : 0x1;
+      uint32_t stage = 0, phase = 0, acc = 0, aphase = 0;
+      for (int u = cid; u < n_units; u += ncl) {
+        const int j = u / p.n_mt;
+        const int t0 = (j * p.n_vt) / n_slices, t1 = ((j + 1) * p.n_vt) / n_slices;
+        for (int vt = t0; vt < t1; ++vt) {
+          mbar_wait(smem_u32(&tempty[acc]), aphase ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + acc * kTileN;
+          for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait(smem_u32(&full[stage]), phase);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(smem_a + stage * C::kABytes);
+            const uint32_t b0 = smem_u32(smem_b + stage * C::kBBytes);
+#pragma unroll
+            for (int k = 0; k < kBlockK / kUmmaK; ++k) {
+              umma_bf16<C::kCtaGroup>(d_tmem, umma_desc_sw128(a0 + k * kUmmaK * 2),
+                                      umma_desc_sw128(b0 + k * kUmmaK * 2), idesc, (kb | k) != 0);
+            }
+            umma_commit_mc<C::kCtaGroup>(smem_u32(&empty[stage]), mask);
+            if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+          }
+          umma_commit_mc<C::kCtaGroup>(smem_u32(&tfull[acc]), mask);
+          acc ^= 1;
+          if (acc == 0) aphase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ===================== epilogue warps: TMEM -> registers -> online LSE =====================
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int row_in_cta = q * 32 + lane;
+    const uint32_t tempty_leader = kPair ? mapa(smem_u32(tempty), 0) : smem_u32(tempty);
+    uint32_t acc = 0, aphase = 0;
+    for (int u = cid; u < n_units; u += ncl) {
+      const int j = u / p.n_mt, mt = u % p.n_mt;
+      const int row = mt * C::kUnitM + rank * kCtaM + row_in_cta;
+      const bool valid = row < p.n_tok;
+      const int64_t a = valid ? __ldg(p.ids + row) : int64_t(-1);
+      const float T = (valid && p.temps) ? __ldg(p.temps + row) : p.temperature;
+      const float c = __fdiv_rn(kLog2eF, T);
+      float m = -CUDART_INF_F, s = 0.f, uu = 0.f, ya = -CUDART_INF_F;
+      const int t0 = (j * p.n_vt) / n_slices, t1 = ((j + 1) * p.n_vt) / n_slices;
+      for (int vt = t0; vt < t1; ++vt) {
+        mbar_wait(smem_u32(&tfull[acc]), aphase);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kTileN;
+        const bool tail_tile = (vt + 1) * kTileN > p.vocab;
+#pragma unroll 1
+        for (int ch = 0; ch < kTileN / 32; ++ch) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(taddr + ch * 32, r);
+          tmem_ld_wait();
+          if (ch == kTileN / 32 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+          }
+          const int col0 = vt * kTileN + ch * 32;
+          if (kDebug && valid) {
+            float* dst = p.debug_logits + static_cast<int64_t>(row) * p.debug_ld + col0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (col0 + i < p.vocab) dst[i] = __uint_as_float(r[i]);
+          }
+          if (tail_tile)
+            epi_chunk<true>(r, c, col0, p.vocab, a, m, s, uu, ya);
+          else
+            epi_chunk<false>(r, c, col0, p.vocab, a, m, s, uu, ya);
+        }
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
+      }
+      if (valid) p.partials[static_cast<int64_t>(j) * p.n_tok + row] = make_float4(m, s, uu, ya);
+    }
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  if (kPair) cluster_sync(); else __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<C::kCtaGroup>(tmem_base, 512);
+  }
+}
+
+// a4: fixed-order merge of the S_v slice partials of every token (fp64), id / temperature checks.
+__global__ void __launch_bounds__(256) logprob_merge_kernel(MergeParams p) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < p.n_tok) {
+    double M = -CUDART_INF;
+    for (int j = 0; j < p.n_slices; ++j) M = fmax(M, static_cast<double>(p.partials[j * p.n_tok + t].x));
+    double S = 0.0, U = 0.0, ya = -CUDART_INF;
+    for (int j = 0; j < p.n_slices; ++j) {
+      const float4 q = p.partials[j * p.n_tok + t];
+      const double dm = static_cast<double>(q.x) - M;
+      const double w = exp2(dm);
+      S = S + static_cast<double>(q.y) * w;
+      U = U + w * (static_cast<double>(q.z) + static_cast<double>(q.y) * dm);
+      if (q.w > -CUDART_INF_F) ya = static_cast<double>(q.w);
+    }
+    const int64_t a = p.ids[t];
+    bool bad = a < 0 || a >= p.vocab;
+    if (p.temps) {
+      const float T = p.temps[t];
+      bad = bad || !(T > 0.f) || !isfinite(T);
+    }
+    const double l2s = log2(S);
+    const double kLn2 = 0.69314718055994530942;
+    p.logp[t] = bad ? CUDART_NAN_F : static_cast<float>(kLn2 * ((ya - M) - l2s));
+    if (p.entropy) p.entropy[t] = static_cast<float>(kLn2 * (l2s - U / S));
+    if (bad) atomicMax(reinterpret_cast<unsigned long long*>(&p.ws->bad_inv),
+                       static_cast<unsigned long long>(kBadSentinel - t));
+  }
+  commit_status_last_block(p.ws, p.dstatus);
+}
+
+template <bool kPair, bool kDebug>
+static cudaError_t launch_fwd(const CUtensorMap& th, const CUtensorMap& tw, const LogprobParams& p, int grid,
+                              cudaStream_t stream) {
+  using C = KCfg<kPair>;
+  auto kern = logprob_fwd_kernel<kPair, kDebug>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kPair ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, th, tw, p);
+}
+
+int fwd_unit_rows(bool pair) { return pair ? KCfg<true>::kUnitM : KCfg<false>::kUnitM; }
+int fwd_w_box_rows(bool pair) { return pair ? KCfg<true>::kBRows : KCfg<false>::kBRows; }
+
+cudaError_t launch_logprob_fwd(bool pair, bool debug, const CUtensorMap& th, const CUtensorMap& tw,
+                               const LogprobParams& p, int grid, cudaStream_t stream) {
+  if (pair) return debug ? launch_fwd<true, true>(th, tw, p, grid, stream) : launch_fwd<true, false>(th, tw, p, grid, stream);
+  return debug ? launch_fwd<false, true>(th, tw, p, grid, stream) : launch_fwd<false, false>(th, tw, p, grid, stream);
+}
+
+cudaError_t launch_logprob_merge(const MergeParams& p, cudaStream_t stream) {
+  const int blocks = static_cast<int>((p.n_tok + 255) / 256);
+  logprob_merge_kernel<<<blocks, 256, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace tim

@@ -1,0 +1,128 @@
+// tim_internal.h -- shared declarations between the C-ABI host layer and the kernels.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/tim.h"
+
+namespace tim {
+
+// Per-call workspace header (memset to 0 before every call).
+struct WsHeader {
+  unsigned long long bad_inv;  // max over bad tokens of (kBadSentinel - index); 0 = no error
+  unsigned int counter;        // "last block" ticket
+  unsigned int pad;
+  unsigned long long reserved[6];
+};
+static_assert(sizeof(WsHeader) == 64, "WsHeader size");
+constexpr unsigned long long kBadSentinel = 1ull << 62;
+constexpr size_t kWsHeaderBytes = 256;
+
+struct LogprobParams {
+  const int64_t* ids;
+  const float* temps;
+  float temperature;
+  float4* partials;  // [n_slices][n_tok]
+  int n_tok;
+  int vocab;
+  int hidden;
+  int n_mt;
+  int n_vt;
+  int n_slices;
+  float* debug_logits;  // test-only raw fp32 accumulators [n_tok][debug_ld]
+  int64_t debug_ld;
+};
+
+struct MergeParams {
+  const float4* partials;
+  const int64_t* ids;
+  const float* temps;
+  float* logp;
+  float* entropy;
+  int64_t n_tok;
+  int vocab;
+  int n_slices;
+  WsHeader* ws;
+  tim_device_status* dstatus;
+};
+
+// Commit the call's data-error state to the caller's status word; executed by the last block
+// of a grid to finish (ticket in ws->counter).  Deterministic: min index wins.
+__device__ __forceinline__ void commit_status_last_block(WsHeader* ws, tim_device_status* st) {
+  __shared__ int last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int ticket = atomicAdd(&ws->counter, 1u);
+    last = (ticket == gridDim.x * gridDim.y * gridDim.z - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0 && st != nullptr) {
+    __threadfence();
+    const unsigned long long b = atomicAdd(&ws->bad_inv, 0ull);
+    if (b != 0) {
+      const int64_t idx = static_cast<int64_t>(kBadSentinel - b);
+      volatile tim_device_status* vs = st;
+      if (vs->code == 0) {
+        vs->first_bad_index = idx;
+        vs->code = TIM_ERR_DATA;
+      } else if (idx < vs->first_bad_index) {
+        vs->first_bad_index = idx;
+      }
+    }
+  }
+}
+
+// logprob.cu
+int fwd_unit_rows(bool pair);
+int fwd_w_box_rows(bool pair);
+cudaError_t launch_logprob_fwd(bool pair, bool debug, const CUtensorMap& th, const CUtensorMap& tw,
+                               const LogprobParams& p, int grid, cudaStream_t stream);
+cudaError_t launch_logprob_merge(const MergeParams& p, cudaStream_t stream);
+
+// correct.cu
+struct CorrectDevCfg {
+  int tis, tok_rs, seq_rs, seq_agg;
+  double tis_cap, log_tis_cap, log_lo, log_hi, tau_seq;
+};
+struct LocalParams {
+  const float* num;
+  const float* den;
+  const int64_t* cu;
+  int64_t n_seq;
+  int64_t tok_begin;
+  int64_t n;
+  const uint8_t* resp;
+  float* tis_w;       // may be null (stats only)
+  uint8_t* tok_keep;  // may be null
+  float* coeff;       // may be null
+  tim_partial_header* hdr;
+  tim_seq_partial* seqp;
+  CorrectDevCfg cfg;
+  tim_device_status* dstatus;
+};
+struct FinishParams {
+  const uint8_t* gathered;  // [nranks][block_bytes]
+  int64_t block_bytes;
+  int nranks;
+  int64_t n_seq;
+  CorrectDevCfg cfg;
+  uint8_t* seq_keep;     // may be null
+  double* seq_score;     // may be null
+  tim_stats* stats;      // may be null
+};
+struct ZeroParams {
+  const int64_t* cu;
+  int64_t n_seq;
+  int64_t tok_begin;
+  int64_t n;
+  const uint8_t* seq_keep;
+  float* coeff;
+};
+cudaError_t launch_correct_local(const LocalParams& p, int num_sms, cudaStream_t stream);
+cudaError_t launch_correct_finish(const FinishParams& p, cudaStream_t stream);
+cudaError_t launch_correct_zero(const ZeroParams& p, cudaStream_t stream);
+
+}  // namespace tim

@@ -1,0 +1,422 @@
+"""ctypes binding of libtim.so (include/tim.h).  Argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; this module converts torch
+tensors into raw device pointers, picks the caller's current CUDA stream, sizes the
+workspaces and maps status codes to exceptions.  Host tensors passed to ``logprob`` /
+``correct`` are copied to the device first and results copied back (the end-to-end form
+bench.py times), which is the only host<->device traffic this module issues.
+
+Method: PAPER.md §2 (delta_t), §4.1 (P:349 recomputation, P:393 K1/K3), §4.2
+(P:496-547 r_corr, L_TIS, L_RS, S_seq), App. A.4 (P:812-896 the four patch objectives,
+tau_tok = 2, tau_seq = 0.001).
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import math
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libtim.so")
+
+TIM_OK = 0
+_STATUS = {0: "TIM_OK", 1: "TIM_ERR_NULL", 2: "TIM_ERR_SHAPE", 3: "TIM_ERR_ALIGN", 4: "TIM_ERR_VALUE",
+           5: "TIM_ERR_WORKSPACE", 6: "TIM_ERR_CUDA", 7: "TIM_ERR_NCCL", 8: "TIM_ERR_UNSUPPORTED",
+           9: "TIM_ERR_DATA"}
+SEQ_NONE, SEQ_K1, SEQ_K3 = 0, 1, 3
+AGG_SUM, AGG_MEAN = 0, 1
+
+
+class TimError(RuntimeError):
+    def __init__(self, code: int, where: str, msg: str = ""):
+        super().__init__(f"{where}: {_STATUS.get(code, code)} {msg}".strip())
+        self.code = code
+
+
+class CorrectCfgC(ctypes.Structure):
+    _fields_ = [("tis", ctypes.c_int32), ("tok_rs", ctypes.c_int32), ("seq_rs", ctypes.c_int32),
+                ("seq_agg", ctypes.c_int32), ("tis_cap", ctypes.c_double), ("log_tis_cap", ctypes.c_double),
+                ("log_tok_lo", ctypes.c_double), ("log_tok_hi", ctypes.c_double), ("tau_seq", ctypes.c_double)]
+
+
+class StatsC(ctypes.Structure):
+    _fields_ = [("n_tok", ctypes.c_int64), ("n_resp_tok", ctypes.c_int64), ("n_seq", ctypes.c_int64),
+                ("n_truncated", ctypes.c_int64), ("n_tok_rejected", ctypes.c_int64),
+                ("n_seq_rejected", ctypes.c_int64), ("n_saturated", ctypes.c_int64),
+                ("sum_abs_delta_fx", ctypes.c_int64 * 2), ("sum_k1_fx", ctypes.c_int64 * 2),
+                ("sum_k3_fx", ctypes.c_int64 * 2), ("max_abs_delta", ctypes.c_double),
+                ("mean_abs_delta", ctypes.c_double), ("mean_k1", ctypes.c_double), ("mean_k3", ctypes.c_double)]
+
+
+STATS_BYTES = ctypes.sizeof(StatsC)  # 136
+PARTIAL_HEADER_BYTES = 128
+SEQ_PARTIAL_BYTES = 32
+
+_P = ctypes.c_void_p
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+_F = ctypes.c_float
+_SZ = ctypes.c_size_t
+
+_SIGS = {
+    "tim_status_string": (ctypes.c_char_p, [_I32]),
+    "tim_abi_version": (ctypes.c_int, []),
+    "tim_logprob_workspace_bytes": (_SZ, [_I64, _I32, _I32]),
+    "tim_logprob_vocab_slices": (_I32, [_I32]),
+    "tim_logprob": (_I32, [_P, _I64, _P, _I32, _I32, _P, _I64, _F, _P, _P, _P, _P, _SZ, _P, _P]),
+    "tim_stats_finalize": (_I32, [_P]),
+    "tim_correct_workspace_bytes": (_SZ, [_I64, _I64, _I32]),
+    "tim_mismatch_stats": (_I32, [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _SZ, _P, _P]),
+    "tim_correct": (_I32, [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P, _P]),
+    "tim_correct_partial_bytes": (_SZ, [_I64]),
+    "tim_correct_local": (_I32, [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "tim_correct_finish": (_I32, [_P, _I32, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P]),
+    "tim_comm_unique_id": (_I32, [_P]),
+    "tim_comm_init": (_I32, [_P, _I32, _I32, ctypes.POINTER(_P)]),
+    "tim_comm_destroy": (_I32, [_P]),
+    "tim_debug_logprob_logits": (_I32, [_P, _I64, _P, _I32, _I32, _P, _I64, _P, _I64, _P, _P, _P, _SZ, _P]),
+    "tim_debug_set_kernel": (_I32, [_I32, _I32]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def lib():
+    """Load libtim.so (fails loudly: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(_LIB_PATH):
+                    raise RuntimeError(f"libtim.so not built ({_LIB_PATH}); run __graft_entry__.build()")
+                L = ctypes.CDLL(_LIB_PATH)
+                for name, (res, args) in _SIGS.items():
+                    fn = getattr(L, name)
+                    fn.restype = res
+                    fn.argtypes = args
+                _lib = L
+    return _lib
+
+
+def _check(code: int, where: str):
+    if code != TIM_OK:
+        raise TimError(code, where, lib().tim_status_string(code).decode())
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def vocab_slices(vocab: int) -> int:
+    return int(lib().tim_logprob_vocab_slices(vocab))
+
+
+# ----------------------------------------------------------------------------------- workspaces --
+_ws_cache: dict = {}
+
+
+def _workspace(device, nbytes: int, tag: str) -> torch.Tensor:
+    key = (str(device), tag)
+    t = _ws_cache.get(key)
+    if t is None or t.numel() < nbytes:
+        t = torch.empty(max(nbytes, 256) + 256, dtype=torch.uint8, device=device)
+        _ws_cache[key] = t
+    return t
+
+
+def new_status(device) -> torch.Tensor:
+    """Zeroed device status word (tim_device_status, 16 B) as int64[2]: [code | reserved<<32, first_bad]."""
+    return torch.zeros(2, dtype=torch.int64, device=device)
+
+
+def read_status(st: torch.Tensor) -> tuple[int, int]:
+    v = st.cpu().tolist()
+    return int(v[0] & 0xFFFFFFFF), int(v[1])
+
+
+# --------------------------------------------------------------------------------------- logprob --
+def logprob(hidden: torch.Tensor, weight: torch.Tensor, ids: torch.Tensor, temperature: float = 1.0,
+            temperatures: torch.Tensor | None = None, entropy: bool = True, out: tuple | None = None,
+            status: torch.Tensor | None = None, device=None):
+    """Per-token log pi(ids[t] | row t) and entropy (nats) -- tim_logprob.
+
+    hidden [N, d] bf16 (rows may be strided), weight [V, d] bf16 contiguous, ids [N] int64.
+    Host (CPU) inputs are copied to ``device`` and the results copied back.
+    """
+    host = not hidden.is_cuda
+    dev = torch.device(device) if device is not None else (hidden.device if not host else torch.device("cuda"))
+    if host:
+        hidden = hidden.to(dev, non_blocking=True)
+        ids = ids.to(dev, non_blocking=True)
+        if temperatures is not None:
+            temperatures = temperatures.to(dev, non_blocking=True)
+    if not weight.is_cuda:
+        weight = weight.to(dev, non_blocking=True)
+    if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
+        raise TypeError("hidden and weight must be bfloat16")
+    if hidden.dim() != 2 or hidden.stride(1) != 1:
+        raise ValueError("hidden must be [N, d] with unit inner stride")
+    weight = weight.contiguous()
+    ids = ids.to(torch.int64).contiguous()
+    N, d = hidden.shape
+    V = weight.shape[0]
+    if weight.shape[1] != d or ids.numel() != N:
+        raise ValueError(f"shape mismatch: hidden {tuple(hidden.shape)}, weight {tuple(weight.shape)}, ids {tuple(ids.shape)}")
+    if temperatures is not None:
+        temperatures = temperatures.to(torch.float32).contiguous()
+    if out is None:
+        lp = torch.empty(N, dtype=torch.float32, device=dev)
+        ent = torch.empty(N, dtype=torch.float32, device=dev) if entropy else None
+    else:
+        lp, ent = out
+    L = lib()
+    wsb = L.tim_logprob_workspace_bytes(N, d, V)
+    ws = _workspace(dev, wsb, "logprob")
+    code = L.tim_logprob(_ptr(hidden), hidden.stride(0), _ptr(weight), d, V, _ptr(ids), N, float(temperature),
+                         _ptr(temperatures), _ptr(lp), _ptr(ent), _ptr(ws), ws.numel(), _ptr(status), _stream(dev))
+    _check(code, "tim_logprob")
+    if host:
+        lp = lp.to("cpu", non_blocking=False)
+        ent = ent.to("cpu") if ent is not None else None
+    return lp, ent
+
+
+def debug_logits(hidden: torch.Tensor, weight: torch.Tensor, ids: torch.Tensor):
+    """TEST ONLY (tim_debug.h): raw fp32 accumulators z = H W^T plus logp / entropy."""
+    N, d = hidden.shape
+    V = weight.shape[0]
+    dev = hidden.device
+    z = torch.full((N, V), float("nan"), dtype=torch.float32, device=dev)
+    lp = torch.empty(N, dtype=torch.float32, device=dev)
+    ent = torch.empty(N, dtype=torch.float32, device=dev)
+    L = lib()
+    ws = _workspace(dev, L.tim_logprob_workspace_bytes(N, d, V), "logprob")
+    _check(L.tim_debug_logprob_logits(_ptr(hidden), hidden.stride(0), _ptr(weight), d, V, _ptr(ids), N, _ptr(z), V,
+                                      _ptr(lp), _ptr(ent), _ptr(ws), ws.numel(), _stream(dev)), "tim_debug_logprob_logits")
+    return z, lp, ent
+
+
+def debug_set_kernel(use_pair: bool = True, max_ctas: int = 0):
+    """TEST ONLY: select the cta_group::2 (contract) or ::1 kernel and cap the persistent grid."""
+    _check(lib().tim_debug_set_kernel(int(use_pair), int(max_ctas)), "tim_debug_set_kernel")
+
+
+# -------------------------------------------------------------------------------- corrections --
+@dataclasses.dataclass
+class CorrectConfig:
+    """tim_correct_cfg.  Paper values: tau_tok = 2, tau_seq = 0.001."""
+
+    tis: bool = False
+    tis_cap: float = 2.0
+    tok_rs: bool = False
+    tok_lo: float = 0.5
+    tok_hi: float = 2.0
+    seq_rs: int = SEQ_NONE
+    seq_agg: int = AGG_SUM
+    tau_seq: float = 1e-3
+
+    def to_c(self) -> CorrectCfgC:
+        return CorrectCfgC(int(self.tis), int(self.tok_rs), int(self.seq_rs), int(self.seq_agg),
+                           float(self.tis_cap), math.log(self.tis_cap), math.log(self.tok_lo),
+                           math.log(self.tok_hi), float(self.tau_seq))
+
+
+# App. A.4.  The masking signal (num, den) is chosen by the caller:
+# *-corr-ratio -> (train_old, rollout); *-ppo-ratio -> (current, rollout).
+PRESETS = {
+    "srs-k3-corr-ratio": CorrectConfig(seq_rs=SEQ_K3, seq_agg=AGG_SUM, tau_seq=1e-3),
+    "srs-k3-ppo-ratio": CorrectConfig(seq_rs=SEQ_K3, seq_agg=AGG_SUM, tau_seq=1e-3),
+    "tis-srs-k3-corr-ratio": CorrectConfig(tis=True, tis_cap=2.0, seq_rs=SEQ_K3, seq_agg=AGG_SUM, tau_seq=1e-3),
+    "tis-srs-k1-corr-ratio": CorrectConfig(tis=True, tis_cap=2.0, seq_rs=SEQ_K1, seq_agg=AGG_SUM, tau_seq=1e-3),
+}
+
+
+def stats_from_bytes(raw: torch.Tensor) -> dict:
+    """Host copy of a device tim_stats (uint8[136]) -> finalized dict (tim_stats_finalize)."""
+    st = StatsC.from_buffer_copy(bytes(raw.cpu().numpy().tobytes()))
+    _check(lib().tim_stats_finalize(ctypes.byref(st)), "tim_stats_finalize")
+
+    def i128(a):
+        return int(a[0]) % (1 << 64) + (int(a[1]) << 64)
+
+    return {
+        "n_tok": st.n_tok, "n_resp_tok": st.n_resp_tok, "n_seq": st.n_seq, "n_truncated": st.n_truncated,
+        "n_tok_rejected": st.n_tok_rejected, "n_seq_rejected": st.n_seq_rejected, "n_saturated": st.n_saturated,
+        "sum_abs_delta": i128(st.sum_abs_delta_fx), "sum_k1": i128(st.sum_k1_fx), "sum_k3": i128(st.sum_k3_fx),
+        "max_abs_delta": st.max_abs_delta, "mean_abs_delta": st.mean_abs_delta, "mean_k1": st.mean_k1,
+        "mean_k3": st.mean_k3,
+    }
+
+
+def _prep_correct(lp_num, lp_den, cu_seqlens, resp_mask, dev):
+    host = not lp_num.is_cuda
+    if host:
+        lp_num = lp_num.to(dev, non_blocking=True)
+        lp_den = lp_den.to(dev, non_blocking=True)
+        if resp_mask is not None:
+            resp_mask = resp_mask.to(dev, non_blocking=True)
+    if not cu_seqlens.is_cuda:
+        cu_seqlens = cu_seqlens.to(dev, non_blocking=True)
+    lp_num = lp_num.to(torch.float32).contiguous()
+    lp_den = lp_den.to(torch.float32).contiguous()
+    cu_seqlens = cu_seqlens.to(torch.int64).contiguous()
+    if resp_mask is not None:
+        resp_mask = resp_mask.to(torch.uint8).contiguous()
+    return host, lp_num, lp_den, cu_seqlens, resp_mask
+
+
+def correct(lp_num: torch.Tensor, lp_den: torch.Tensor, cu_seqlens: torch.Tensor, cfg: CorrectConfig,
+            resp_mask: torch.Tensor | None = None, tok_begin: int = 0, comm: "Comm | None" = None,
+            status: torch.Tensor | None = None, return_stats: bool = True, device=None, out: dict | None = None):
+    """TIS / token-RS / sequence-RS coefficients and statistics -- tim_correct.
+
+    Returns dict(tis_w, tok_keep, seq_keep, coeff, seq_score, stats_raw[, stats]).  With
+    ``return_stats`` the device stats are copied to the host (this synchronizes)."""
+    dev = torch.device(device) if device is not None else (lp_num.device if lp_num.is_cuda else torch.device("cuda"))
+    host, lp_num, lp_den, cu_seqlens, resp_mask = _prep_correct(lp_num, lp_den, cu_seqlens, resp_mask, dev)
+    n = lp_num.numel()
+    S = cu_seqlens.numel() - 1
+    nranks = comm.nranks if comm is not None else 1
+    if out is None:
+        out = {
+            "tis_w": torch.empty(n, dtype=torch.float32, device=dev),
+            "tok_keep": torch.empty(n, dtype=torch.uint8, device=dev),
+            "seq_keep": torch.empty(S, dtype=torch.uint8, device=dev),
+            "coeff": torch.empty(n, dtype=torch.float32, device=dev),
+            "seq_score": torch.empty(S, dtype=torch.float64, device=dev),
+            "stats_raw": torch.zeros(STATS_BYTES, dtype=torch.uint8, device=dev),
+        }
+    L = lib()
+    ws = _workspace(dev, L.tim_correct_workspace_bytes(n, S, nranks), "correct")
+    c = cfg.to_c()
+    code = L.tim_correct(_ptr(lp_num), _ptr(lp_den), _ptr(cu_seqlens), S, int(tok_begin), n, _ptr(resp_mask),
+                         ctypes.byref(c), comm.handle if comm is not None else None, _ptr(out["tis_w"]),
+                         _ptr(out["tok_keep"]), _ptr(out["seq_keep"]), _ptr(out["coeff"]), _ptr(out["seq_score"]),
+                         _ptr(out["stats_raw"]), _ptr(ws), ws.numel(), _ptr(status), _stream(dev))
+    _check(code, "tim_correct")
+    res = dict(out)
+    if return_stats:
+        res["stats"] = stats_from_bytes(out["stats_raw"])
+    if host:
+        res = {k: (v.cpu() if isinstance(v, torch.Tensor) else v) for k, v in res.items()}
+    return res
+
+
+def mismatch_stats(lp_num, lp_den, cu_seqlens, resp_mask=None, tok_begin: int = 0, comm=None, status=None,
+                   device=None) -> dict:
+    """delta statistics only -- tim_mismatch_stats (synchronizes to return host values)."""
+    dev = torch.device(device) if device is not None else (lp_num.device if lp_num.is_cuda else torch.device("cuda"))
+    _, lp_num, lp_den, cu_seqlens, resp_mask = _prep_correct(lp_num, lp_den, cu_seqlens, resp_mask, dev)
+    n = lp_num.numel()
+    S = cu_seqlens.numel() - 1
+    nranks = comm.nranks if comm is not None else 1
+    L = lib()
+    ws = _workspace(dev, L.tim_correct_workspace_bytes(n, S, nranks), "correct")
+    raw = torch.zeros(STATS_BYTES, dtype=torch.uint8, device=dev)
+    _check(L.tim_mismatch_stats(_ptr(lp_num), _ptr(lp_den), _ptr(cu_seqlens), S, int(tok_begin), n, _ptr(resp_mask),
+                                comm.handle if comm is not None else None, _ptr(raw), _ptr(ws), ws.numel(),
+                                _ptr(status), _stream(dev)), "tim_mismatch_stats")
+    return stats_from_bytes(raw)
+
+
+def partial_bytes(n_seq: int) -> int:
+    return int(lib().tim_correct_partial_bytes(n_seq))
+
+
+def correct_local(lp_num, lp_den, cu_seqlens, cfg: CorrectConfig, resp_mask=None, tok_begin: int = 0,
+                  status=None):
+    """Split form, pass 1: per-token outputs + this rank's exact partial block (uint8 tensor)."""
+    dev = lp_num.device
+    _, lp_num, lp_den, cu_seqlens, resp_mask = _prep_correct(lp_num, lp_den, cu_seqlens, resp_mask, dev)
+    n = lp_num.numel()
+    S = cu_seqlens.numel() - 1
+    tis_w = torch.empty(n, dtype=torch.float32, device=dev)
+    tok_keep = torch.empty(n, dtype=torch.uint8, device=dev)
+    coeff = torch.empty(n, dtype=torch.float32, device=dev)
+    part = torch.empty(partial_bytes(S), dtype=torch.uint8, device=dev)
+    c = cfg.to_c()
+    _check(lib().tim_correct_local(_ptr(lp_num), _ptr(lp_den), _ptr(cu_seqlens), S, int(tok_begin), n,
+                                   _ptr(resp_mask), ctypes.byref(c), _ptr(tis_w), _ptr(tok_keep), _ptr(coeff),
+                                   _ptr(part), _ptr(status), _stream(dev)), "tim_correct_local")
+    return {"tis_w": tis_w, "tok_keep": tok_keep, "coeff": coeff, "partial": part}
+
+
+def exchange_partials(partial: torch.Tensor, group=None) -> tuple[torch.Tensor, int]:
+    """All-gather every rank's partial block, in rank order, over torch.distributed (plumbing only:
+    the blocks are exact integers, so any collective algorithm gives identical bits)."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return partial, 1
+    world = dist.get_world_size(group)
+    if world == 1:
+        return partial, 1
+    gathered = torch.empty(world * partial.numel(), dtype=partial.dtype, device=partial.device)
+    dist.all_gather_into_tensor(gathered, partial, group=group)
+    return gathered, world
+
+
+def correct_finish(gathered: torch.Tensor, nranks: int, cu_seqlens, cfg: CorrectConfig, coeff: torch.Tensor,
+                   tok_begin: int = 0):
+    """Split form, pass 2: exact combine, sequence decisions, coeff zeroing, stats."""
+    dev = coeff.device
+    cu = cu_seqlens.to(dev).to(torch.int64).contiguous()
+    S = cu.numel() - 1
+    seq_keep = torch.empty(S, dtype=torch.uint8, device=dev)
+    seq_score = torch.empty(S, dtype=torch.float64, device=dev)
+    raw = torch.zeros(STATS_BYTES, dtype=torch.uint8, device=dev)
+    c = cfg.to_c()
+    _check(lib().tim_correct_finish(_ptr(gathered), int(nranks), _ptr(cu), S, int(tok_begin), coeff.numel(),
+                                    ctypes.byref(c), _ptr(coeff), _ptr(seq_keep), _ptr(seq_score), _ptr(raw),
+                                    _stream(dev)), "tim_correct_finish")
+    return {"seq_keep": seq_keep, "seq_score": seq_score, "stats_raw": raw}
+
+
+def shard_range(n_tok: int, nranks: int, rank: int, align: int = 256) -> tuple[int, int]:
+    """Token range [a, b) of `rank`: floor(r N / P) rounded down to `align` (balance only; correctness
+    never depends on where the cut falls -- sequences may straddle ranks)."""
+    if nranks < 1 or not (0 <= rank < nranks):
+        raise ValueError("bad rank")
+
+    def cut(r):
+        if r >= nranks:
+            return n_tok
+        c = (r * n_tok) // nranks
+        return min(n_tok, (c // align) * align)
+
+    return cut(rank), cut(rank + 1)
+
+
+class Comm:
+    """NCCL communicator owned by libtim (tim_comm_init); bootstrap via torch.distributed."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group)
+        self.nranks = dist.get_world_size(group)
+        uid = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _check(lib().tim_comm_unique_id(uid), "tim_comm_unique_id")
+        obj = [bytes(uid.raw)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        uid = ctypes.create_string_buffer(obj[0], 128)
+        h = ctypes.c_void_p()
+        _check(lib().tim_comm_init(uid, self.nranks, self.rank, ctypes.byref(h)), "tim_comm_init")
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            lib().tim_comm_destroy(self.handle)
+            self.handle = None

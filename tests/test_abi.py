@@ -1,0 +1,128 @@
+"""CPU-only checks of the C ABI (no compute call needs a GPU here).
+
+The library must load, export every symbol include/tim.h and include/tim_debug.h declare, and
+reject bad arguments synchronously before touching the device (tim.h "Conventions").
+"""
+import ctypes
+import math
+import os
+import re
+
+import pytest
+
+from paper_2605_14220_b200 import tim
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    names = set()
+    for h in ("tim.h", "tim_debug.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        names |= set(re.findall(r"\b(tim_[a-z0-9_]+)\s*\(", src))
+    return names
+
+
+@pytest.fixture(scope="module")
+def L():
+    return tim.lib()
+
+
+def test_exports_every_declared_symbol(L):
+    names = _declared()
+    assert {"tim_logprob", "tim_mismatch_stats", "tim_correct", "tim_comm_init", "tim_comm_destroy",
+            "tim_stats_finalize"} <= names
+    for n in sorted(names):
+        assert hasattr(L, n), n
+        assert n in tim._SIGS, f"binding lacks a signature for {n}"
+
+
+def test_version_and_strings(L):
+    assert L.tim_abi_version() == 1
+    for code in range(10):
+        assert L.tim_status_string(code).decode().startswith(tim._STATUS[code])
+
+
+def test_workspace_sizes(L):
+    assert L.tim_logprob_vocab_slices(151936) == 8
+    assert L.tim_logprob_vocab_slices(1024) == 4      # 4 tiles of 256 -> 4 slices
+    assert L.tim_logprob_vocab_slices(1) == 1
+    assert L.tim_logprob_workspace_bytes(1000, 2048, 151936) == 256 + 8 * 1000 * 16
+    assert L.tim_correct_partial_bytes(5) == 128 + 5 * 32
+    assert L.tim_correct_workspace_bytes(100, 5, 1) == 512
+    assert L.tim_correct_workspace_bytes(100, 5, 4) == 512 * 5
+
+
+P = ctypes.c_void_p
+
+
+def _lp(L, hidden=P(4096), ld=256, weight=P(8192), d=256, V=1024, ids=P(16), n=10, T=1.0, out=P(32),
+        ws=P(1 << 20), wsb=1 << 30):
+    return L.tim_logprob(hidden, ld, weight, d, V, ids, n, T, None, out, None, ws, wsb, None, None)
+
+
+def test_logprob_argument_errors_are_synchronous(L):
+    assert _lp(L, hidden=None) == 1
+    assert _lp(L, ids=None) == 1
+    assert _lp(L, d=200, ld=200) == 2            # hidden % 64
+    assert _lp(L, V=0) == 2
+    assert _lp(L, n=-1) == 2
+    assert _lp(L, ld=128) == 2                    # ld_hidden < hidden
+    assert _lp(L, T=0.0) == 4 and _lp(L, T=float("nan")) == 4
+    assert _lp(L, hidden=P(4104)) == 3            # not 16-B aligned
+    assert _lp(L, ld=260) == 3                    # pitch*2 % 16
+    assert _lp(L, n=0) == 0                       # empty batch: no launch
+    assert _lp(L, wsb=100) == 5
+
+
+def _cfg(**kw):
+    c = tim.CorrectConfig(**kw).to_c()
+    return c
+
+
+def test_correct_argument_errors_are_synchronous(L):
+    c = _cfg(seq_rs=tim.SEQ_K3)
+    args = dict(num=P(4096), den=P(8192), cu=P(16), S=2, tb=0, n=10, resp=None)
+
+    def call(cfg=c, **kw):
+        a = dict(args, **kw)
+        return L.tim_correct_local(a["num"], a["den"], a["cu"], a["S"], a["tb"], a["n"], a["resp"],
+                                   ctypes.byref(cfg) if cfg is not None else None, None, None, None,
+                                   P(1 << 16), None, None)
+
+    assert call(num=None) == 1
+    assert call(cfg=None) == 1
+    assert call(n=-3) == 2
+    assert call(S=0) == 2
+    assert call(num=P(4100)) == 3
+    bad = _cfg(seq_rs=tim.SEQ_K3, tau_seq=2000.0)
+    assert call(cfg=bad) == 4
+    bad2 = _cfg(tok_rs=True, tok_lo=2.0, tok_hi=1.0)
+    assert call(cfg=bad2) == 4
+    bad3 = tim.CorrectCfgC(0, 0, 2, 0, 2.0, math.log(2), 0, 0, 1e-3)   # seq_rs = 2 is not a tim_seq_rs
+    assert call(cfg=bad3) == 4
+
+
+def test_stats_finalize_rounding(L):
+    st = tim.StatsC()
+    st.n_resp_tok = 3
+    big = (1 << 90) + 12345
+    st.sum_abs_delta_fx[0] = ctypes.c_int64(big & ((1 << 64) - 1) if big & (1 << 63) == 0 else (big & ((1 << 64) - 1)) - (1 << 64)).value
+    st.sum_abs_delta_fx[1] = big >> 64
+    neg = -(3 << 52) - 1
+    st.sum_k1_fx[0] = ctypes.c_int64(neg).value
+    st.sum_k1_fx[1] = -1
+    assert L.tim_stats_finalize(ctypes.byref(st)) == 0
+    assert st.mean_abs_delta == (float(big) * 2.0 ** -52) / 3
+    assert st.mean_k1 == (float(neg) * 2.0 ** -52) / 3
+    assert st.mean_k3 == 0.0
+
+
+def test_shard_range_covers_tokens():
+    for n in (0, 1, 255, 256, 1000, 262144, 8388609):
+        for P_ in (1, 2, 3, 4, 8):
+            cuts = [tim.shard_range(n, P_, r) for r in range(P_)]
+            assert cuts[0][0] == 0 and cuts[-1][1] == n
+            for (a, b), (c, d) in zip(cuts[:-1], cuts[1:]):
+                assert b == c and a <= b
