@@ -363,6 +363,10 @@ def exchange_partials(partial: torch.Tensor, group=None) -> tuple[torch.Tensor, 
     world = dist.get_world_size(group)
     if world == 1:
         return partial, 1
+    if dist.get_backend(group) == "gloo":  # gloo lacks all_gather_into_tensor on some builds
+        parts = [torch.empty_like(partial) for _ in range(world)]
+        dist.all_gather(parts, partial, group=group)
+        return torch.cat(parts), world
     gathered = torch.empty(world * partial.numel(), dtype=partial.dtype, device=partial.device)
     dist.all_gather_into_tensor(gathered, partial, group=group)
     return gathered, world
