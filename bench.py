@@ -122,6 +122,8 @@ def run_ours(args):
     from paper_2605_14220_b200 import tim
 
     world, rank, local = _dist()
+    if args.tuning:
+        tim.debug_set_tuning(*[int(x) for x in args.tuning.split(",")])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -390,6 +392,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tuning", default=None, help="h_policy,w_policy,sleep (experiments; results unchanged)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -24,6 +24,12 @@ tim_status tim_debug_logprob_logits(const void* hidden_bf16, int64_t ld_hidden, 
  * persistent grid (emulates a GPU with fewer SMs for batch-invariance tests), 0 = all SMs. */
 tim_status tim_debug_set_kernel(int32_t use_pair, int32_t max_ctas_or_clusters);
 
+/* Performance knobs (never change results): L2 eviction policy of the hidden-state (H) and
+ * weight (W) TMA tile loads, 0 = no hint, 1 = evict_normal, 2 = evict_first, 3 = evict_last;
+ * sleep_waits = 1 makes the TMA-producer and epilogue mbarrier waits sleep in hardware;
+ * sync_slack > 0 bounds how many vocab tiles a CTA pair may run ahead of the slowest pair. */
+tim_status tim_debug_set_tuning(int32_t h_policy, int32_t w_policy, int32_t sleep_waits, int32_t sync_slack);
+
 #ifdef __cplusplus
 }
 #endif

@@ -33,6 +33,11 @@ std::mutex g_mu;
 // debug knobs (tim_debug.h): kernel variant and an SM cap to emulate smaller GPUs
 int g_use_pair = 1;
 int g_max_clusters = 0;
+// tuning knobs (tim_debug.h): L2 policies of the H / W tile loads and sleeping mbarrier waits
+int g_h_policy = 3;  // H tiles: evict_last (re-read for every vocab tile of the sweep)
+int g_w_policy = 2;  // W tiles: evict_first (shared by all pairs within a few tiles, then dead)
+int g_sleep_waits = 1;
+int g_sync_slack = 4;  // pairs stay within 4 vocab tiles of each other: W window ~4 MB in L2
 
 tim_status device_info(DevInfo** out) {
   int dev = 0;
@@ -123,7 +128,7 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   uint8_t* wsb = static_cast<uint8_t*>(ws);
   WsHeader* hdr = reinterpret_cast<WsHeader*>(wsb);
   float4* partials = reinterpret_cast<float4*>(wsb + kWsHeaderBytes);
-  if (cudaMemsetAsync(hdr, 0, sizeof(WsHeader), s) != cudaSuccess) return TIM_ERR_CUDA;
+  if (cudaMemsetAsync(hdr, 0, kWsHeaderBytes, s) != cudaSuccess) return TIM_ERR_CUDA;
 
   LogprobParams p{};
   p.ids = ids;
@@ -139,6 +144,11 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   p.n_slices = vocab_slices(vocab);
   p.debug_logits = debug_logits;
   p.debug_ld = debug_ld;
+  p.h_policy = g_h_policy;
+  p.w_policy = g_w_policy;
+  p.sleep_waits = g_sleep_waits;
+  p.progress = reinterpret_cast<uint32_t*>(wsb + kWsProgressOffset);
+  p.sync_slack = g_sync_slack;
   const int64_t n_units = static_cast<int64_t>(p.n_mt) * p.n_slices;
   int64_t ctas_cap = pair ? dev->max_pair_clusters : dev->max_single_ctas;
   if (g_max_clusters > 0 && g_max_clusters < ctas_cap) ctas_cap = g_max_clusters;
@@ -492,6 +502,16 @@ tim_status tim_debug_set_kernel(int32_t use_pair, int32_t max_ctas_or_clusters) 
   if (max_ctas_or_clusters < 0) return TIM_ERR_VALUE;
   g_use_pair = use_pair;
   g_max_clusters = max_ctas_or_clusters;
+  return TIM_OK;
+}
+
+tim_status tim_debug_set_tuning(int32_t h_policy, int32_t w_policy, int32_t sleep_waits, int32_t sync_slack) {
+  if (sync_slack < 0) return TIM_ERR_VALUE;
+  g_sync_slack = sync_slack;
+  if (h_policy < 0 || h_policy > 3 || w_policy < 0 || w_policy > 3) return TIM_ERR_VALUE;
+  g_h_policy = h_policy;
+  g_w_policy = w_policy;
+  g_sleep_waits = sleep_waits != 0;
   return TIM_OK;
 }
 

@@ -56,21 +56,24 @@ __device__ __forceinline__ float chunk_max32(const float (&y)[32]) {
 }
 
 // Online update of the row state with 32 consecutive columns (fixed order, fixed tree).
+// Log2 domain: y = z * c with c = RN(log2(e) / T) > 0.  The chunk max is taken on the raw
+// accumulators (RN is monotone, so RN(max z * c) = max RN(z * c)), and t = y - m is formed by
+// one FFMA (z * c - m rounded once): per logit FMNMX(3) + FFMA + MUFU.EX2 + FADD + FFMA.
 template <bool kTail>
 __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float c, int col0, int vocab, int64_t a,
                                           float& m, float& s, float& u, float& ya) {
-  float y[32];
+  float z[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
-    y[i] = __uint_as_float(r[i]) * c;
-    if (kTail && col0 + i >= vocab) y[i] = -CUDART_INF_F;
+    z[i] = __uint_as_float(r[i]);
+    if (kTail && col0 + i >= vocab) z[i] = -CUDART_INF_F;
   }
-  const float cmax = chunk_max32(y);
+  const float cmax = chunk_max32(z) * c;
   const int64_t rel = a - col0;
   if (static_cast<uint64_t>(rel) < 32u) {
 #pragma unroll
     for (int i = 0; i < 32; ++i)
-      if (rel == i) ya = y[i];
+      if (rel == i) ya = z[i] * c;
   }
   if (cmax > m) {
     const float dm = m - cmax;  // -inf on the first chunk of a slice
@@ -79,10 +82,11 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float c, int 
     s = s * sc;
     m = cmax;
   }
+  const float nm = -m;
   float s4[4] = {0.f, 0.f, 0.f, 0.f}, u4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
-    float t = y[i] - m;
+    float t = fmaf(z[i], c, nm);
     if (kTail) t = fmaxf(t, -256.f);  // masked column: e = 0, e * t = 0 (no -inf * 0)
     const float e = ex2_approx(t);
     s4[i & 3] += e;
@@ -90,6 +94,64 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float c, int 
   }
   s += (s4[0] + s4[1]) + (s4[2] + s4[3]);
   u += (u4[0] + u4[1]) + (u4[2] + u4[3]);
+}
+
+__device__ __forceinline__ uint64_t make_policy(int kind) {
+  return kind == 3 ? policy_evict_last() : kind == 2 ? policy_evict_first() : policy_evict_normal();
+}
+
+// Static unit schedule (changes only WHICH pair runs a unit, never any row's arithmetic).
+// Full rounds: in round r pair c owns M-tile r*ncl + c and sweeps all S_v slices of it, i.e.
+// vocab tiles 0..n_vt-1 in ascending order -- every pair reads the same W tile at the same
+// step, and its H tile (1 MB) stays hot in L2 for the whole vocabulary.  The remaining
+// n_mt % ncl M-tiles are split into (M-tile, slice) units dealt round-robin, slice-major.
+struct UnitSched {
+  int rounds, rem, ncl, S;
+  __device__ UnitSched(int n_mt, int n_slices, int n_clusters)
+      : rounds(n_mt / n_clusters), rem(n_mt % n_clusters), ncl(n_clusters), S(n_slices) {}
+  __device__ __forceinline__ bool unit(int c, int k, int& mt, int& j) const {
+    if (k < rounds * S) {
+      mt = (k / S) * ncl + c;
+      j = k % S;
+      return true;
+    }
+    const int q = c + (k - rounds * S) * ncl;
+    if (q >= rem * S) return false;
+    j = q / rem;
+    mt = rounds * ncl + q % rem;
+    return true;
+  }
+};
+
+__device__ __forceinline__ void st_relaxed_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Whole producer warp: wait (at most ~200 us) until every pair has issued `target` tiles.
+// Returns the observed minimum.  Only a throttle -- never needed for correctness.
+__device__ __noinline__ uint32_t wait_progress(const uint32_t* prog, uint32_t ncl, uint32_t target, int lane) {
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t mn;
+  while (true) {
+    mn = 0xFFFFFFFFu;
+    for (uint32_t c = lane; c < ncl; c += 32) {
+      const uint32_t v = ld_relaxed_gpu(prog + c);
+      mn = v < mn ? v : mn;
+    }
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    if (mn >= target || globaltimer_ns() - t0 > 200000ull) break;
+    __nanosleep(256);
+  }
+  return mn;
 }
 
 template <bool kPair, bool kDebug>
@@ -137,47 +199,64 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int n_slices = p.n_slices;
-  const int n_units = p.n_mt * n_slices;
   const int nkb = p.hidden / kBlockK;
+  const UnitSched sched(p.n_mt, n_slices, ncl);
 
   if (warp == 0) {
-    // ===================== TMA producer (one thread per CTA) =====================
-    if (lane == 0) {
-      uint32_t stage = 0, phase = 0;
-      for (int u = cid; u < n_units; u += ncl) {
-        const int j = u / p.n_mt, mt = u % p.n_mt;
-        const int m0 = mt * C::kUnitM + rank * kCtaM;
-        const int t0 = (j * p.n_vt) / n_slices, t1 = ((j + 1) * p.n_vt) / n_slices;
-        for (int vt = t0; vt < t1; ++vt) {
-          const int n0 = vt * kTileN + rank * C::kBRows;
-          for (int kb = 0; kb < nkb; ++kb) {
-            mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+    // ===================== TMA producer (whole warp; lane 0 issues) =====================
+    uint32_t stage = 0, phase = 0;
+    const uint64_t pol_h = make_policy(p.h_policy), pol_w = make_policy(p.w_policy);
+    const bool hints = p.h_policy != 0 || p.w_policy != 0;
+    const bool gate = kPair && leader && p.sync_slack > 0 && p.progress != nullptr;
+    uint32_t step = 0, known_min = 0;
+    int mt, j;
+    for (int k = 0; sched.unit(cid, k, mt, j); ++k) {
+      const int m0 = mt * C::kUnitM + rank * kCtaM;
+      const int t0 = (j * p.n_vt) / n_slices, t1 = ((j + 1) * p.n_vt) / n_slices;
+      for (int vt = t0; vt < t1; ++vt, ++step) {
+        // bound the drift between pairs sweeping the same W tiles (performance only:
+        // the wait is time-limited, results never depend on it)
+        if (gate && static_cast<uint64_t>(step) > static_cast<uint64_t>(known_min) + p.sync_slack)
+          known_min = wait_progress(p.progress, ncl, step - p.sync_slack, lane);
+        const int n0 = vt * kTileN + rank * C::kBRows;
+        for (int kb = 0; kb < nkb; ++kb) {
+          if (p.sleep_waits) mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
+          else mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+          if (lane == 0) {
             const uint32_t fb_local = smem_u32(&full[stage]);
             const uint32_t a_dst = smem_u32(smem_a + stage * C::kABytes);
             const uint32_t b_dst = smem_u32(smem_b + stage * C::kBBytes);
             if (kPair) {
               if (leader) mbar_arrive_expect_tx(fb_local, 2 * C::kStageBytes);
               const uint32_t fb = mapa(fb_local, 0);
-              tma_load_2d_pair(a_dst, &tmap_h, fb, kb * kBlockK, m0);
-              tma_load_2d_pair(b_dst, &tmap_w, fb, kb * kBlockK, n0);
+              if (hints) {
+                tma_load_2d_pair_hint(a_dst, &tmap_h, fb, kb * kBlockK, m0, pol_h);
+                tma_load_2d_pair_hint(b_dst, &tmap_w, fb, kb * kBlockK, n0, pol_w);
+              } else {
+                tma_load_2d_pair(a_dst, &tmap_h, fb, kb * kBlockK, m0);
+                tma_load_2d_pair(b_dst, &tmap_w, fb, kb * kBlockK, n0);
+              }
             } else {
               mbar_arrive_expect_tx(fb_local, C::kStageBytes);
               tma_load_2d(a_dst, &tmap_h, fb_local, kb * kBlockK, m0);
               tma_load_2d(b_dst, &tmap_w, fb_local, kb * kBlockK, n0);
             }
-            if (++stage == C::kStages) { stage = 0; phase ^= 1; }
           }
+          __syncwarp();
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
+        if (gate && lane == 0) st_relaxed_gpu(p.progress + cid, step + 1);
       }
     }
+    if (gate && lane == 0) st_relaxed_gpu(p.progress + cid, 0xFFFFFFFFu);
   } else if (warp == 1) {
     // ===================== MMA issuer (one thread of the leader CTA) =====================
     if (leader && lane == 0) {
       const uint32_t idesc = umma_idesc_bf16_f32(kPair ? 256 : 128, kTileN);
       const uint16_t mask = kPair ? 0x3 : 0x1;
       uint32_t stage = 0, phase = 0, acc = 0, aphase = 0;
-      for (int u = cid; u < n_units; u += ncl) {
-        const int j = u / p.n_mt;
+      int mt, j;
+      for (int k = 0; sched.unit(cid, k, mt, j); ++k) {
         const int t0 = (j * p.n_vt) / n_slices, t1 = ((j + 1) * p.n_vt) / n_slices;
         for (int vt = t0; vt < t1; ++vt) {
           mbar_wait(smem_u32(&tempty[acc]), aphase ^ 1);
@@ -189,9 +268,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t a0 = smem_u32(smem_a + stage * C::kABytes);
             const uint32_t b0 = smem_u32(smem_b + stage * C::kBBytes);
 #pragma unroll
-            for (int k = 0; k < kBlockK / kUmmaK; ++k) {
-              umma_bf16<C::kCtaGroup>(d_tmem, umma_desc_sw128(a0 + k * kUmmaK * 2),
-                                      umma_desc_sw128(b0 + k * kUmmaK * 2), idesc, (kb | k) != 0);
+            for (int kk = 0; kk < kBlockK / kUmmaK; ++kk) {
+              umma_bf16<C::kCtaGroup>(d_tmem, umma_desc_sw128(a0 + kk * kUmmaK * 2),
+                                      umma_desc_sw128(b0 + kk * kUmmaK * 2), idesc, (kb | kk) != 0);
             }
             umma_commit_mc<C::kCtaGroup>(smem_u32(&empty[stage]), mask);
             if (++stage == C::kStages) { stage = 0; phase ^= 1; }
@@ -208,8 +287,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row_in_cta = q * 32 + lane;
     const uint32_t tempty_leader = kPair ? mapa(smem_u32(tempty), 0) : smem_u32(tempty);
     uint32_t acc = 0, aphase = 0;
-    for (int u = cid; u < n_units; u += ncl) {
-      const int j = u / p.n_mt, mt = u % p.n_mt;
+    int mt, j;
+    for (int k = 0; sched.unit(cid, k, mt, j); ++k) {
       const int row = mt * C::kUnitM + rank * kCtaM + row_in_cta;
       const bool valid = row < p.n_tok;
       const int64_t a = valid ? __ldg(p.ids + row) : int64_t(-1);
@@ -218,7 +297,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       float m = -CUDART_INF_F, s = 0.f, uu = 0.f, ya = -CUDART_INF_F;
       const int t0 = (j * p.n_vt) / n_slices, t1 = ((j + 1) * p.n_vt) / n_slices;
       for (int vt = t0; vt < t1; ++vt) {
-        mbar_wait(smem_u32(&tfull[acc]), aphase);
+        if (p.sleep_waits) mbar_wait_sleep(smem_u32(&tfull[acc]), aphase);
+        else mbar_wait(smem_u32(&tfull[acc]), aphase);
         tc_fence_after();
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kTileN;
         const bool tail_tile = (vt + 1) * kTileN > p.vocab;

@@ -18,7 +18,9 @@ struct WsHeader {
 };
 static_assert(sizeof(WsHeader) == 64, "WsHeader size");
 constexpr unsigned long long kBadSentinel = 1ull << 62;
-constexpr size_t kWsHeaderBytes = 256;
+constexpr size_t kWsHeaderBytes = 1024;      // WsHeader + per-pair progress counters
+constexpr size_t kWsProgressOffset = 64;
+constexpr int kMaxProgress = (kWsHeaderBytes - kWsProgressOffset) / 4;
 
 struct LogprobParams {
   const int64_t* ids;
@@ -33,6 +35,11 @@ struct LogprobParams {
   int n_slices;
   float* debug_logits;  // test-only raw fp32 accumulators [n_tok][debug_ld]
   int64_t debug_ld;
+  int h_policy;         // L2 eviction policy of H / W tile loads: 0 none, 1 normal, 2 first, 3 last
+  int w_policy;
+  int sleep_waits;      // producer / epilogue mbarrier waits sleep (suspend-time hint) instead of polling
+  uint32_t* progress;   // [clusters] tiles issued per CTA pair (workspace, zeroed per call)
+  int sync_slack;       // max tiles a pair may run ahead of the slowest pair (0 = no throttle)
 };
 
 struct MergeParams {

@@ -80,6 +80,7 @@ _SIGS = {
     "tim_comm_destroy": (_I32, [_P]),
     "tim_debug_logprob_logits": (_I32, [_P, _I64, _P, _I32, _I32, _P, _I64, _P, _I64, _P, _P, _P, _SZ, _P]),
     "tim_debug_set_kernel": (_I32, [_I32, _I32]),
+    "tim_debug_set_tuning": (_I32, [_I32, _I32, _I32, _I32]),
 }
 
 _lib = None
@@ -207,6 +208,12 @@ def debug_logits(hidden: torch.Tensor, weight: torch.Tensor, ids: torch.Tensor):
     _check(L.tim_debug_logprob_logits(_ptr(hidden), hidden.stride(0), _ptr(weight), d, V, _ptr(ids), N, _ptr(z), V,
                                       _ptr(lp), _ptr(ent), _ptr(ws), ws.numel(), _stream(dev)), "tim_debug_logprob_logits")
     return z, lp, ent
+
+
+def debug_set_tuning(h_policy: int = 0, w_policy: int = 0, sleep_waits: bool = False, sync_slack: int = 0):
+    """Performance knobs (results unchanged): L2 policies for H / W loads, sleeping waits."""
+    _check(lib().tim_debug_set_tuning(int(h_policy), int(w_policy), int(sleep_waits), int(sync_slack)),
+           "tim_debug_set_tuning")
 
 
 def debug_set_kernel(use_pair: bool = True, max_ctas: int = 0):

@@ -151,10 +151,11 @@ def test_pair_and_single_cta_variants_agree_within_tolerance(tim):
 
 def test_special_cases(tim):
     d = 128
-    # V = 1: logp = 0 and H = 0 exactly
+    # V = 1: logp = 0 and H = 0 (exact in the oracle; on the GPU t = fma(z, c, -RN(z c)) is the
+    # rounding error of one fp32 product, so the result is 0 to within ~1e-8)
     H, W, ids = _case(300, d, 1, 9)
     lp, ent = tim.logprob(H, W, torch.zeros(300, dtype=torch.int64, device=DEV))
-    assert torch.all(lp == 0) and torch.all(ent == 0)
+    assert lp.abs().max().item() < 1e-6 and ent.abs().max().item() < 1e-6
     # W == 0: uniform, logp = -ln V, H = ln V
     for V in (2, 257, 151936):
         Wz = torch.zeros(V, d, dtype=torch.bfloat16, device=DEV)
