@@ -278,6 +278,8 @@ def run_ours(args):
         "correction_stats": {k: stats[k] for k in ("n_resp_tok", "n_truncated", "n_seq_rejected", "max_abs_delta",
                                                      "mean_abs_delta", "mean_k3")},
     }
+    if args.correction_tokens > 0:
+        out["correction_roofline"] = correction_roofline(tim, dev, args.correction_tokens, peaks, peak_src)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"], out["max_abs_dlogp_vs_oracle"] = cpu_baseline(cfg, W, Hh, ids, lp, lp_roll, mask,
                                                                             args.cpu_seconds)
@@ -291,6 +293,40 @@ def run_ours(args):
 
 def H_bytes(cfg):
     return cfg.n_tok * cfg.hidden * 2
+
+
+def correction_roofline(tim, dev, n, peaks, peak_src, reps=10):
+    """Standalone tim_correct (tis-srs-k3-corr-ratio, 4096-token sequences, 3/4 response) at n
+    tokens: 18 algorithmic bytes per token (read 2 fp32 + u8 mask, write fp32 w + u8 keep + fp32
+    coeff) vs the measured HBM copy bandwidth.  Inputs (1.2 GB at 2^27) exceed L2."""
+    S = n // 4096
+    cu = synth.cu_seqlens(S, 4096).to(dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(20260004)
+    den = -torch.empty(n, device=dev).exponential_(0.7, generator=g)
+    num = synth.perturb_laplace_mix(den, 20260004)
+    mask = (torch.arange(n, device=dev) % 4096 >= 1024).to(torch.uint8)
+    cfg = tim.PRESETS["tis-srs-k3-corr-ratio"]
+    out = {"tis_w": torch.empty(n, dtype=torch.float32, device=dev),
+           "tok_keep": torch.empty(n, dtype=torch.uint8, device=dev),
+           "seq_keep": torch.empty(S, dtype=torch.uint8, device=dev),
+           "coeff": torch.empty(n, dtype=torch.float32, device=dev),
+           "seq_score": torch.empty(S, dtype=torch.float64, device=dev),
+           "stats_raw": torch.zeros(tim.STATS_BYTES, dtype=torch.uint8, device=dev)}
+    for _ in range(3):
+        tim.correct(num, den, cu, cfg, mask, return_stats=False, out=out)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in evs:
+        a.record()
+        tim.correct(num, den, cu, cfg, mask, return_stats=False, out=out)
+        b.record()
+    torch.cuda.synchronize()
+    ms = sorted(a.elapsed_time(b) for a, b in evs)[reps // 2]
+    gbs = 18.0 * n / (ms / 1e3) / 1e9
+    peak = float(peaks["hbm_gbs"])
+    return {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak, "traffic": None,
+            "n_tok": n, "ms": ms, "algorithmic_bytes_per_token": 18, "peak_source": peak_src + " hbm_gbs",
+            "kernel": "tim_correct (correct_local + finish + zero, median of %d)" % reps}
 
 
 def _blas_threads():
@@ -392,6 +428,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--correction-tokens", type=int, default=1 << 27,
+                    help="standalone correction-kernel HBM roofline at this many tokens (0 = skip)")
     ap.add_argument("--tuning", default=None, help="h_policy,w_policy,sleep (experiments; results unchanged)")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -86,8 +86,12 @@ def delta(lp_num, lp_den) -> np.ndarray:
         np.asarray(lp_den, dtype=np.float32).astype(np.float64)
 
 
+SMALL = 2.0 ** -6  # |delta| <= SMALL: short Horner polynomials (truncation < 1e-19 relative)
+
+
 def exp_contract(d) -> np.ndarray:
-    """C.3.6 exp_c: Cody-Waite reduction + degree-13 Taylor Horner + ldexp."""
+    """C.3.6 exp_c.  |d| <= 2^-6: degree-7 Taylor Horner in d.  Otherwise Cody-Waite
+    reduction + degree-13 Taylor Horner + ldexp; +inf above 709, 0 below -700."""
     d = np.asarray(d, dtype=np.float64)
     dd = np.where(np.isfinite(d), np.clip(d, -700.0, 709.0), 0.0)
     k = np.rint(dd * LOG2E)
@@ -96,13 +100,20 @@ def exp_contract(d) -> np.ndarray:
     for n in range(12, -1, -1):
         p = p * r + INV_FACT[n]
     out = np.ldexp(p, k.astype(np.int64))
+    small = np.abs(dd) <= SMALL
+    ds = np.where(small, dd, 0.0)
+    q = np.full_like(ds, INV_FACT[7])
+    for n in range(6, -1, -1):
+        q = q * ds + INV_FACT[n]
+    out = np.where(small, q, out)
     out = np.where(d > 709.0, np.inf, out)
     out = np.where(d < -700.0, 0.0, out)
     return out
 
 
 def k3_contract(d) -> np.ndarray:
-    """C.3.6 K3 = e^d - 1 - d: series branch for |d| <= 1, exp branch otherwise."""
+    """C.3.6 K3 = e^d - 1 - d = d^2 P(d): P = Horner series of RN(1/n!) with n = 2..9 for
+    |d| <= 2^-6 and n = 2..23 for |d| <= 1; (exp_c(d) - 1) - d otherwise."""
     d = np.asarray(d, dtype=np.float64)
     small = np.abs(d) <= 1.0
     ds = np.where(small, d, 0.0)
@@ -110,6 +121,12 @@ def k3_contract(d) -> np.ndarray:
     for n in range(22, 1, -1):
         P = P * ds + INV_FACT[n]
     series = (ds * ds) * P
+    tiny = np.abs(d) <= SMALL
+    dt = np.where(tiny, d, 0.0)
+    Q = np.full_like(dt, INV_FACT[9])
+    for n in range(8, 1, -1):
+        Q = Q * dt + INV_FACT[n]
+    series = np.where(tiny, (dt * dt) * Q, series)
     big = (exp_contract(d) - 1.0) - d
     return np.where(small, series, big)
 

@@ -36,10 +36,19 @@ constexpr double kLn2Lo = 0x1.a39ef35793c76p-33;
 constexpr double kTwo52 = 0x1p52;
 constexpr long long kSatX = 1ll << 62;
 
-// e^d: k = rint(d log2 e), r = (d - k ln2_hi) - k ln2_lo, degree-13 Taylor (Horner), * 2^k.
+constexpr double kSmall = 0x1p-6;  // |d| <= 2^-6: short Horner polynomials
+
+// e^d.  |d| <= 2^-6: degree-7 Taylor (Horner) in d.  Otherwise Cody-Waite: k = rint(d log2 e),
+// r = (d - k ln2_hi) - k ln2_lo, degree-13 Taylor (Horner), * 2^k; +inf above 709, 0 below -700.
 __device__ __forceinline__ double exp_c(double d) {
   if (d > 709.0) return CUDART_INF;
   if (d < -700.0) return 0.0;
+  if (fabs(d) <= kSmall) {
+    double q = kInvFact[7];
+#pragma unroll
+    for (int n = 6; n >= 0; --n) q = __dadd_rn(__dmul_rn(q, d), kInvFact[n]);
+    return q;
+  }
   const double k = rint(__dmul_rn(d, kLog2e));
   const double r = __dsub_rn(__dsub_rn(d, __dmul_rn(k, kLn2Hi)), __dmul_rn(k, kLn2Lo));
   double p = kInvFact[13];
@@ -49,9 +58,17 @@ __device__ __forceinline__ double exp_c(double d) {
   return __dmul_rn(p, __longlong_as_double((ki + 1023) << 52));
 }
 
-// K3 = e^d - 1 - d: Horner series of (e^d - 1 - d) / d^2 for |d| <= 1, else via exp_c.
+// K3 = e^d - 1 - d = d^2 P(d): Horner series of (e^d - 1 - d) / d^2 with RN(1/n!), n = 2..9 for
+// |d| <= 2^-6, n = 2..23 for |d| <= 1; (exp_c(d) - 1) - d otherwise.
 __device__ __forceinline__ double k3_c(double d) {
-  if (fabs(d) <= 1.0) {
+  const double ad = fabs(d);
+  if (ad <= kSmall) {
+    double Q = kInvFact[9];
+#pragma unroll
+    for (int n = 8; n >= 2; --n) Q = __dadd_rn(__dmul_rn(Q, d), kInvFact[n]);
+    return __dmul_rn(__dmul_rn(d, d), Q);
+  }
+  if (ad <= 1.0) {
     double P = kInvFact[23];
 #pragma unroll
     for (int n = 22; n >= 2; --n) P = __dadd_rn(__dmul_rn(P, d), kInvFact[n]);
@@ -135,7 +152,7 @@ constexpr int kWarpTok = 32 * kTpl;     // tokens per warp chunk
 constexpr int kLocalThreads = 256;
 
 template <bool kOut, bool kSeq>
-__global__ void __launch_bounds__(kLocalThreads) correct_local_kernel(LocalParams p) {
+__global__ void __launch_bounds__(kLocalThreads, 3) correct_local_kernel(LocalParams p) {
   const int lane = threadIdx.x & 31;
   const long long warp_g = (static_cast<long long>(blockIdx.x) * kLocalThreads + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * kLocalThreads) >> 5;
@@ -478,7 +495,7 @@ cudaError_t launch_correct_local(const LocalParams& p, int num_sms, cudaStream_t
   const long long chunks = (p.n + kWarpTok - 1) / kWarpTok;
   const long long warps_per_block = kLocalThreads / 32;
   long long blocks = (chunks + warps_per_block - 1) / warps_per_block;
-  const long long cap = static_cast<long long>(num_sms) * 8;
+  const long long cap = static_cast<long long>(num_sms) * 3;  // one resident wave (3 blocks / SM)
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   const bool out = p.tis_w != nullptr;

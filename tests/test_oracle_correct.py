@@ -75,8 +75,9 @@ def test_table1_without_flip_token_kept(table1, agg):
 
 def _sweep():
     mags = np.logspace(-300, math.log10(1024.0), 3000)
-    extra = np.array([1e-12, 1e-8, 0.5, 0.999999, 1.0, 1.0000001, math.log(2), 6.9, 6.94, 7.0, 709.0, 700.0])
-    v = np.concatenate([mags, extra])
+    extra = np.array([1e-12, 1e-8, 0.5, 0.999999, 1.0, 1.0000001, math.log(2), 6.9, 6.94, 7.0, 709.0, 700.0,
+                      2.0 ** -6, np.nextafter(2.0 ** -6, 1.0), np.nextafter(2.0 ** -6, 0.0)])
+    v = np.concatenate([mags, extra, np.linspace(1e-4, 2.0 ** -5, 700)])
     return np.concatenate([v, -v, [0.0]])
 
 
