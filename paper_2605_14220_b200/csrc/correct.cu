@@ -152,7 +152,7 @@ constexpr int kWarpTok = 32 * kTpl;     // tokens per warp chunk
 constexpr int kLocalThreads = 256;
 
 template <bool kOut, bool kSeq>
-__global__ void __launch_bounds__(kLocalThreads, 3) correct_local_kernel(LocalParams p) {
+__global__ void __launch_bounds__(kLocalThreads, 2) correct_local_kernel(LocalParams p) {
   const int lane = threadIdx.x & 31;
   const long long warp_g = (static_cast<long long>(blockIdx.x) * kLocalThreads + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * kLocalThreads) >> 5;
@@ -164,7 +164,23 @@ __global__ void __launch_bounds__(kLocalThreads, 3) correct_local_kernel(LocalPa
   unsigned long long maxbits = 0;
   unsigned long long bad_inv = 0;
 
-  for (long long ch = warp_g; ch < n_chunks; ch += nwarps) {
+  // every warp owns a contiguous run of chunks: one binary search per lane per run, then the
+  // per-lane sequence accumulator walks forward (flushing only when it crosses a boundary)
+  const long long cpw = (n_chunks + nwarps - 1) / nwarps;
+  const long long c_begin = warp_g * cpw;
+  const long long c_end = c_begin + cpw < n_chunks ? c_begin + cpw : n_chunks;
+  SeqAcc acc;
+  acc.sid = LLONG_MAX;
+  acc.x = 0;
+  acc.t = 0;
+  acc.nsat = 0;
+  long long next_b = LLONG_MAX;
+  if (kSeq && c_begin < c_end && c_begin * kWarpTok + lane * kTpl < p.n) {
+    acc.sid = seq_of(p.cu, p.n_seq, p.tok_begin + c_begin * kWarpTok + lane * kTpl);
+    next_b = __ldg(p.cu + acc.sid + 1);
+  }
+
+  for (long long ch = c_begin; ch < c_end; ++ch) {
     const long long i0 = ch * kWarpTok + lane * kTpl;
     float num[kTpl], den[kTpl];
     uint8_t rs[kTpl];
@@ -197,15 +213,41 @@ __global__ void __launch_bounds__(kLocalThreads, 3) correct_local_kernel(LocalPa
       }
     }
 
-    SeqAcc acc;
-    acc.sid = LLONG_MAX;
-    acc.x = 0;
-    acc.t = 0;
-    acc.nsat = 0;
-    long long next_b = 0;
-    if (kSeq && i0 < p.n) {
-      acc.sid = seq_of(p.cu, p.n_seq, p.tok_begin + i0);
-      next_b = __ldg(p.cu + acc.sid + 1);
+    // (1) delta for the lane's 8 tokens; (2) the short small-|delta| polynomials of all 8 tokens in
+    // lockstep (8 independent Horner chains: latency hidden by ILP); (3) the rare tokens outside
+    // [-2^-6, 2^-6] take the long contract paths.  Same op sequence per token as exp_c / k3_c.
+    double dv[kTpl], ds[kTpl], ev[kTpl], k3v[kTpl];
+    unsigned big_mask = 0;
+#pragma unroll
+    for (int k = 0; k < kTpl; ++k) {
+      dv[k] = __dsub_rn(static_cast<double>(num[k]), static_cast<double>(den[k]));
+      const bool ok = i0 + k < p.n && isfinite(dv[k]);
+      const bool sm = ok && fabs(dv[k]) <= kSmall;
+      if (ok && !sm) big_mask |= 1u << k;
+      ds[k] = sm ? dv[k] : 0.0;
+      k3v[k] = kInvFact[9];
+      ev[k] = kInvFact[7];
+    }
+#pragma unroll
+    for (int n = 8; n >= 2; --n)
+#pragma unroll
+      for (int k = 0; k < kTpl; ++k) k3v[k] = __dadd_rn(__dmul_rn(k3v[k], ds[k]), kInvFact[n]);
+#pragma unroll
+    for (int k = 0; k < kTpl; ++k) k3v[k] = __dmul_rn(__dmul_rn(ds[k], ds[k]), k3v[k]);
+    if (cfg.tis) {
+#pragma unroll
+      for (int n = 6; n >= 0; --n)
+#pragma unroll
+        for (int k = 0; k < kTpl; ++k) ev[k] = __dadd_rn(__dmul_rn(ev[k], ds[k]), kInvFact[n]);
+    }
+    if (big_mask) {
+#pragma unroll
+      for (int k = 0; k < kTpl; ++k) {
+        if ((big_mask >> k) & 1u) {
+          k3v[k] = k3_c(dv[k]);
+          if (cfg.tis) ev[k] = exp_c(dv[k]);
+        }
+      }
     }
 
     float w_out[kTpl], c_out[kTpl];
@@ -218,7 +260,7 @@ __global__ void __launch_bounds__(kLocalThreads, 3) correct_local_kernel(LocalPa
       k_out[k] = 1;
       if (i >= p.n) continue;
       const long long g = p.tok_begin + i;
-      const double d = __dsub_rn(static_cast<double>(num[k]), static_cast<double>(den[k]));
+      const double d = dv[k];
       if (!isfinite(d)) {  // C.3.2 data error: excluded from every sum, outputs NaN / 0
         const unsigned long long b = kBadSentinel - static_cast<unsigned long long>(g);
         bad_inv = b > bad_inv ? b : bad_inv;
@@ -229,7 +271,7 @@ __global__ void __launch_bounds__(kLocalThreads, 3) correct_local_kernel(LocalPa
       const bool resp = rs[k] != 0;
       const bool trunc = cfg.tis && d > cfg.log_tis_cap;
       if (cfg.tis) {
-        const double w = trunc ? cfg.tis_cap : fmin(exp_c(d), cfg.tis_cap);
+        const double w = trunc ? cfg.tis_cap : fmin(ev[k], cfg.tis_cap);
         w_out[k] = __double2float_rn(w);
       }
       const bool keep = cfg.tok_rs ? (cfg.log_lo <= d && d <= cfg.log_hi) : true;
@@ -238,7 +280,7 @@ __global__ void __launch_bounds__(kLocalThreads, 3) correct_local_kernel(LocalPa
 
       bool sat_abs, sat1, sat3;
       const long long x1 = fixed_point(-d, sat1);
-      const double k3 = k3_c(d);
+      const double k3 = k3v[k];
       const long long x3 = fixed_point(k3, sat3);
       if (resp) {
         const long long xa = fixed_point(fabs(d), sat_abs);
@@ -295,26 +337,27 @@ __global__ void __launch_bounds__(kLocalThreads, 3) correct_local_kernel(LocalPa
       }
     }
 
-    if (kSeq) {
-      // segmented warp reduction of the open segments (sequence ids are non-decreasing in lane order)
+  }
+
+  if (kSeq) {
+    // segmented warp reduction of the open segments (sequence ids are non-decreasing in lane order)
 #pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const long long osid = __shfl_down_sync(0xffffffffu, acc.sid, off);
-        const __int128 ox = shfl_down_i128(acc.x, off);
-        const long long ot = __shfl_down_sync(0xffffffffu, acc.t, off);
-        const long long on = __shfl_down_sync(0xffffffffu, acc.nsat, off);
-        if (lane + off < 32 && osid == acc.sid) {
-          acc.x += ox;
-          acc.t += ot;
-          acc.nsat += on;
-        }
+    for (int off = 1; off < 32; off <<= 1) {
+      const long long osid = __shfl_down_sync(0xffffffffu, acc.sid, off);
+      const __int128 ox = shfl_down_i128(acc.x, off);
+      const long long ot = __shfl_down_sync(0xffffffffu, acc.t, off);
+      const long long on = __shfl_down_sync(0xffffffffu, acc.nsat, off);
+      if (lane + off < 32 && osid == acc.sid) {
+        acc.x += ox;
+        acc.t += ot;
+        acc.nsat += on;
       }
-      // note: lane l now holds the sum of lanes [l, l+2^k) with the same id, so the head of each
-      // run (first lane of that id) holds the whole run because runs are contiguous.
-      const long long prev_sid = __shfl_up_sync(0xffffffffu, acc.sid, 1);
-      const bool head = lane == 0 || prev_sid != acc.sid;
-      if (head && acc.sid != LLONG_MAX) flush_seq(p.seqp, acc);
     }
+    // note: lane l now holds the sum of lanes [l, l+2^k) with the same id, so the head of each
+    // run (first lane of that id) holds the whole run because runs are contiguous.
+    const long long prev_sid = __shfl_up_sync(0xffffffffu, acc.sid, 1);
+    const bool head = lane == 0 || prev_sid != acc.sid;
+    if (head && acc.sid != LLONG_MAX) flush_seq(p.seqp, acc);
   }
 
   // block reduction of the global statistics, then one set of integer atomics per block
@@ -495,7 +538,7 @@ cudaError_t launch_correct_local(const LocalParams& p, int num_sms, cudaStream_t
   const long long chunks = (p.n + kWarpTok - 1) / kWarpTok;
   const long long warps_per_block = kLocalThreads / 32;
   long long blocks = (chunks + warps_per_block - 1) / warps_per_block;
-  const long long cap = static_cast<long long>(num_sms) * 3;  // one resident wave (3 blocks / SM)
+  const long long cap = static_cast<long long>(num_sms) * 2;  // one resident wave (2 blocks / SM)
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   const bool out = p.tis_w != nullptr;
