@@ -123,13 +123,21 @@ def run_ours(args):
 
     world, rank, local = _dist()
     if args.tuning:
-        tim.debug_set_tuning(*[int(x) for x in args.tuning.split(",")])
+        vals = [int(x) for x in args.tuning.split(",")]
+        tim.debug_set_tuning(*vals[:4])
+        if len(vals) > 4:
+            tim.debug_set_group(vals[4])
+    if args.max_pairs:
+        tim.debug_set_kernel(True, args.max_pairs)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     cfg = synth.CONFIGS[args.config]
+    if args.n_seq:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, n_seq=args.n_seq)
     W, H, ids = build_workload(cfg, rank, dev)
     N = cfg.n_tok
     S_local = cfg.n_seq
@@ -430,7 +438,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--correction-tokens", type=int, default=1 << 27,
                     help="standalone correction-kernel HBM roofline at this many tokens (0 = skip)")
-    ap.add_argument("--tuning", default=None, help="h_policy,w_policy,sleep (experiments; results unchanged)")
+    ap.add_argument("--tuning", default=None,
+                    help="h_policy,w_policy,sleep,slack[,group] (experiments; results unchanged)")
+    ap.add_argument("--max-pairs", type=int, default=0, help="cap the persistent grid (experiments)")
+    ap.add_argument("--n-seq", type=int, default=0, help="override the number of sequences (experiments)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -25,6 +25,7 @@ struct DevInfo {
   int num_sms = 0;
   int max_pair_clusters = 0;
   int max_single_ctas = 0;
+  int l2_bytes = 0;
 };
 constexpr int kMaxDev = 64;
 DevInfo g_dev[kMaxDev];
@@ -38,6 +39,7 @@ int g_h_policy = 3;  // H tiles: evict_last (re-read for every vocab tile of the
 int g_w_policy = 2;  // W tiles: evict_first (shared by all pairs within a few tiles, then dead)
 int g_sleep_waits = 1;
 int g_sync_slack = 4;  // pairs stay within 4 vocab tiles of each other: W window ~4 MB in L2
+int g_group = 0;       // pairs per M-tile group (0 = automatic from the L2 size)
 
 tim_status device_info(DevInfo** out) {
   int dev = 0;
@@ -52,6 +54,7 @@ tim_status device_info(DevInfo** out) {
     d.sm100 = (maj == 10 && min == 0);
     d.max_pair_clusters = d.num_sms / 2;
     d.max_single_ctas = d.num_sms;
+    if (cudaDeviceGetAttribute(&d.l2_bytes, cudaDevAttrL2CacheSize, dev) != cudaSuccess) return TIM_ERR_CUDA;
     d.ok = true;
   }
   *out = &d;
@@ -154,6 +157,18 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   if (g_max_clusters > 0 && g_max_clusters < ctas_cap) ctas_cap = g_max_clusters;
   const int64_t groups = n_units < ctas_cap ? n_units : ctas_cap;
   const int grid = static_cast<int>(groups * (pair ? 2 : 1));
+  // Pairs sharing an M-tile: smallest G in {1, 2, 4, 8} (dividing S_v, <= #pairs) whose live H
+  // tiles (one 256-row tile per group) fit in ~75% of L2.  Performance only: which pair runs
+  // which (M-tile, slice) unit never changes a row's arithmetic.
+  p.group = 1;
+  if (pair && g_group > 0) {
+    if (p.n_slices % g_group == 0 && groups >= g_group) p.group = g_group;
+  } else if (pair) {
+    const double h_tile = 256.0 * d * 2.0;
+    while (p.group < 8 && p.n_slices % (p.group * 2) == 0 && groups >= p.group * 2 &&
+           (static_cast<double>(groups) / p.group) * h_tile > 0.75 * dev->l2_bytes)
+      p.group *= 2;
+  }
   if (launch_logprob_fwd(pair, debug_logits != nullptr, th, tw, p, grid, s) != cudaSuccess) return TIM_ERR_CUDA;
 
   MergeParams mp{};
@@ -502,6 +517,12 @@ tim_status tim_debug_set_kernel(int32_t use_pair, int32_t max_ctas_or_clusters) 
   if (max_ctas_or_clusters < 0) return TIM_ERR_VALUE;
   g_use_pair = use_pair;
   g_max_clusters = max_ctas_or_clusters;
+  return TIM_OK;
+}
+
+tim_status tim_debug_set_group(int32_t group) {
+  if (group != 0 && group != 1 && group != 2 && group != 4 && group != 8) return TIM_ERR_VALUE;
+  g_group = group;
   return TIM_OK;
 }
 

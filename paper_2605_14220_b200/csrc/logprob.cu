@@ -101,24 +101,31 @@ __device__ __forceinline__ uint64_t make_policy(int kind) {
 }
 
 // Static unit schedule (changes only WHICH pair runs a unit, never any row's arithmetic).
-// Full rounds: in round r pair c owns M-tile r*ncl + c and sweeps all S_v slices of it, i.e.
-// vocab tiles 0..n_vt-1 in ascending order -- every pair reads the same W tile at the same
-// step, and its H tile (1 MB) stays hot in L2 for the whole vocabulary.  The remaining
-// n_mt % ncl M-tiles are split into (M-tile, slice) units dealt round-robin, slice-major.
+// Pairs form groups of G (G | S_v): in full round r, group q owns M-tile r*ngrp + q and its
+// member g sweeps slices [g S_v/G, (g+1) S_v/G) -- vocab tiles in ascending order, so all pairs
+// with the same g read the same W tile at the same step, and the ngrp live H tiles (1 MB each at
+// d = 2048: G = 1; 2 MB at d = 4096: G = 2 keeps 74 MB live) stay hot in L2 for the whole sweep.
+// The remaining M-tiles are split into (M-tile, slice) units dealt round-robin, slice-major.
 struct UnitSched {
-  int rounds, rem, ncl, S;
-  __device__ UnitSched(int n_mt, int n_slices, int n_clusters)
-      : rounds(n_mt / n_clusters), rem(n_mt % n_clusters), ncl(n_clusters), S(n_slices) {}
+  int rounds, rem, ncl, S, G, ngrp, per_round;
+  __device__ UnitSched(int n_mt, int n_slices, int n_clusters, int group)
+      : ncl(n_clusters), S(n_slices), G(group) {
+    ngrp = n_clusters / group;
+    rounds = n_mt / ngrp;
+    rem = n_mt - rounds * ngrp;
+    per_round = n_slices / group;
+  }
   __device__ __forceinline__ bool unit(int c, int k, int& mt, int& j) const {
-    if (k < rounds * S) {
-      mt = (k / S) * ncl + c;
-      j = k % S;
+    const int kfull = c < ngrp * G ? rounds * per_round : 0;
+    if (k < kfull) {
+      mt = (k / per_round) * ngrp + c / G;
+      j = (c % G) * per_round + k % per_round;
       return true;
     }
-    const int q = c + (k - rounds * S) * ncl;
+    const int q = c + (k - kfull) * ncl;
     if (q >= rem * S) return false;
     j = q / rem;
-    mt = rounds * ncl + q % rem;
+    mt = rounds * ngrp + q % rem;
     return true;
   }
 };
@@ -200,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int n_slices = p.n_slices;
   const int nkb = p.hidden / kBlockK;
-  const UnitSched sched(p.n_mt, n_slices, ncl);
+  const UnitSched sched(p.n_mt, n_slices, ncl, p.group);
 
   if (warp == 0) {
     // ===================== TMA producer (whole warp; lane 0 issues) =====================

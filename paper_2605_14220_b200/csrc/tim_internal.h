@@ -40,6 +40,7 @@ struct LogprobParams {
   int sleep_waits;      // producer / epilogue mbarrier waits sleep (suspend-time hint) instead of polling
   uint32_t* progress;   // [clusters] tiles issued per CTA pair (workspace, zeroed per call)
   int sync_slack;       // max tiles a pair may run ahead of the slowest pair (0 = no throttle)
+  int group;            // pairs sharing one M-tile (split its slices) so the live H tiles fit in L2
 };
 
 struct MergeParams {
