@@ -338,7 +338,7 @@ size_t tim_correct_workspace_bytes(int64_t n_tok_local, int64_t n_seq, int32_t n
   (void)n_tok_local;
   if (n_seq < 0 || nranks < 1) return 0;
   const size_t b = (tim_correct_partial_bytes(n_seq) + 255) & ~size_t(255);
-  return b * (1 + (nranks > 1 ? static_cast<size_t>(nranks) : 0));
+  return b * (1 + static_cast<size_t>(nranks));  // local block + the all-gathered blocks
 }
 
 tim_status tim_correct_local(const float* num, const float* den, const int64_t* cu, int64_t n_seq,
@@ -431,7 +431,7 @@ static tim_status correct_impl(const float* num, const float* den, const int64_t
                               dstatus, stream)) != TIM_OK)
     return st;
   const void* gathered = local;
-  if (nranks > 1) {
+  if (comm != nullptr) {  // NCCL all-gather of the exact partial blocks (also for a 1-rank comm)
     NcclApi* api = nccl();
     if (!api->ok) return TIM_ERR_NCCL;
     uint8_t* g = local + blk;

@@ -50,7 +50,7 @@ def test_workspace_sizes(L):
     assert L.tim_logprob_vocab_slices(1) == 1
     assert L.tim_logprob_workspace_bytes(1000, 2048, 151936) == 1024 + 8 * 1000 * 16
     assert L.tim_correct_partial_bytes(5) == 128 + 5 * 32
-    assert L.tim_correct_workspace_bytes(100, 5, 1) == 512
+    assert L.tim_correct_workspace_bytes(100, 5, 1) == 512 * 2
     assert L.tim_correct_workspace_bytes(100, 5, 4) == 512 * 5
 
 

@@ -163,3 +163,28 @@ def test_c3_scale_bit_exact(tim):
         res = tim.correct(num.to(DEV), den.to(DEV), cu.to(DEV), c, mask.to(DEV))
         ref = oc.correct(num.numpy(), den.numpy(), cu.numpy(), _ocfg(c), mask.numpy())
         _compare(res, ref, c)
+
+
+def test_nccl_comm_path_single_rank(tim):
+    """tim_correct through a libtim-owned NCCL communicator (world size 1 on this one-GPU box):
+    exercises tim_comm_unique_id / tim_comm_init / ncclAllGather / tim_comm_destroy and must give
+    the same bits as the comm-less call."""
+    import os
+    import torch.distributed as dist
+    own = not dist.is_initialized()
+    if own:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        comm = tim.Comm()
+        num, den, cu, mask = _inputs(9, 600, 21)
+        c = tim.CorrectConfig(tis=True, seq_rs=oc.SEQ_K3, seq_agg=oc.AGG_MEAN, tau_seq=1e-3)
+        a = tim.correct(num.to(DEV), den.to(DEV), cu.to(DEV), c, mask.to(DEV))
+        b = tim.correct(num.to(DEV), den.to(DEV), cu.to(DEV), c, mask.to(DEV), comm=comm)
+        for k in ("tis_w", "tok_keep", "seq_keep", "coeff", "seq_score", "stats_raw"):
+            assert torch.equal(a[k], b[k]), k
+        comm.close()
+    finally:
+        if own:
+            dist.destroy_process_group()
