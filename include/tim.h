@@ -110,6 +110,31 @@ tim_status tim_logprob(const void* hidden_bf16, int64_t ld_hidden,
 int32_t tim_logprob_vocab_slices(int32_t vocab);
 
 /* ----------------------------------------------------------------------------
+ * tim_sample  (the rollout-side twin)
+ *
+ * Samples a_t ~ softmax(z_t / T_t) for every row, with the same head arithmetic as
+ * tim_logprob, so the rollout's log pi(a_t) is produced by the very kernel the trainer uses:
+ * logp_out[t] and entropy_out[t] are bit-identical to what tim_logprob returns for
+ * ids = ids_out (zero training-inference mismatch at the head, §3.1).
+ * Rule (U22): Gumbel-max, a_t = argmax_v x_v + g_v, g_v = -ln(-ln u_v),
+ * u_v = ((x >> 9) + 1/2) 2^-23 with x word (v % 4) of Philox4x32-10(counter = {v / 4, 0,
+ * row_keys[t] lo, row_keys[t] hi}, key = seed); ties go to the lowest column.  The draw of a
+ * row depends only on (seed, row_keys[t], the row's logits): batch-invariant like the log-prob.
+ *   row_keys [n_tok] uint64 (device): per-row counter, e.g. (sequence id << 32) | position.
+ *   ids_out [n_tok] int64, logp_out [n_tok] fp32, entropy_out_or_null [n_tok] fp32.
+ *   workspace >= tim_sample_workspace_bytes(n_tok, hidden, vocab).
+ * Other arguments, constraints and errors as tim_logprob.
+ * -------------------------------------------------------------------------- */
+size_t tim_sample_workspace_bytes(int64_t n_tok, int32_t hidden, int32_t vocab);
+tim_status tim_sample(const void* hidden_bf16, int64_t ld_hidden,
+                      const void* weight_bf16, int32_t hidden, int32_t vocab,
+                      const uint64_t* row_keys, int64_t n_tok, uint64_t seed,
+                      float temperature, const float* temperatures_or_null,
+                      int64_t* ids_out, float* logp_out, float* entropy_out_or_null,
+                      void* workspace, size_t workspace_bytes,
+                      tim_device_status* dstatus, void* stream);
+
+/* ----------------------------------------------------------------------------
  * Corrections and statistics
  *
  * Inputs common to tim_mismatch_stats / tim_correct / tim_correct_local:

@@ -104,7 +104,9 @@ inline int32_t vocab_slices(int32_t vocab) {
 tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weight, int32_t d, int32_t vocab,
                         const int64_t* ids, int64_t n_tok, float temperature, const float* temps, float* logp,
                         float* ent, void* ws, size_t ws_bytes, tim_device_status* dstatus, void* stream,
-                        float* debug_logits, int64_t debug_ld) {
+                        float* debug_logits, int64_t debug_ld, const uint64_t* row_keys = nullptr,
+                        uint64_t seed = 0, int64_t* ids_out = nullptr) {
+  const bool sample = row_keys != nullptr;
   if (!weight) return TIM_ERR_NULL;
   if (n_tok < 0 || n_tok >= (int64_t(1) << 31)) return TIM_ERR_SHAPE;
   if (d < 64 || d > 16384 || d % 64 != 0) return TIM_ERR_SHAPE;
@@ -113,11 +115,12 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   if (!(temperature > 0.f) || !std::isfinite(temperature)) return TIM_ERR_VALUE;
   if (!aligned(weight, 16) || (ld_hidden * 2) % 16 != 0) return TIM_ERR_ALIGN;
   if (n_tok == 0) return TIM_OK;  // empty batch: pointers may be NULL, nothing is launched
-  if (!hidden || !ids || !logp) return TIM_ERR_NULL;
+  if (!hidden || !logp || (sample ? !ids_out : !ids)) return TIM_ERR_NULL;
   if (!aligned(hidden, 16)) return TIM_ERR_ALIGN;
   if (!ws) return TIM_ERR_NULL;
   if (!aligned(ws, 16)) return TIM_ERR_ALIGN;
-  if (ws_bytes < tim_logprob_workspace_bytes(n_tok, d, vocab)) return TIM_ERR_WORKSPACE;
+  if (ws_bytes < (sample ? tim_sample_workspace_bytes(n_tok, d, vocab) : tim_logprob_workspace_bytes(n_tok, d, vocab)))
+    return TIM_ERR_WORKSPACE;
   DevInfo* dev = nullptr;
   tim_status st = device_info(&dev);
   if (st != TIM_OK) return st;
@@ -152,6 +155,9 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   p.sleep_waits = g_sleep_waits;
   p.progress = reinterpret_cast<uint32_t*>(wsb + kWsProgressOffset);
   p.sync_slack = g_sync_slack;
+  p.row_keys = row_keys;
+  p.seed = seed;
+  p.partials2 = sample ? partials + static_cast<size_t>(vocab_slices(vocab)) * static_cast<size_t>(n_tok) : nullptr;
   const int64_t n_units = static_cast<int64_t>(p.n_mt) * p.n_slices;
   int64_t ctas_cap = pair ? dev->max_pair_clusters : dev->max_single_ctas;
   if (g_max_clusters > 0 && g_max_clusters < ctas_cap) ctas_cap = g_max_clusters;
@@ -169,7 +175,8 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
            (static_cast<double>(groups) / p.group) * h_tile > 0.75 * dev->l2_bytes)
       p.group *= 2;
   }
-  if (launch_logprob_fwd(pair, debug_logits != nullptr, th, tw, p, grid, s) != cudaSuccess) return TIM_ERR_CUDA;
+  if (launch_logprob_fwd(pair, debug_logits != nullptr, sample, th, tw, p, grid, s) != cudaSuccess)
+    return TIM_ERR_CUDA;
 
   MergeParams mp{};
   mp.partials = partials;
@@ -182,7 +189,9 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   mp.n_slices = p.n_slices;
   mp.ws = hdr;
   mp.dstatus = dstatus;
-  if (launch_logprob_merge(mp, s) != cudaSuccess) return TIM_ERR_CUDA;
+  mp.partials2 = p.partials2;
+  mp.ids_out = ids_out;
+  if ((sample ? launch_sample_merge(mp, s) : launch_logprob_merge(mp, s)) != cudaSuccess) return TIM_ERR_CUDA;
   return TIM_OK;
 }
 
@@ -301,6 +310,25 @@ tim_status tim_logprob(const void* hidden_bf16, int64_t ld_hidden, const void* w
   return logprob_impl(hidden_bf16, ld_hidden, weight_bf16, hidden, vocab, token_ids, n_tok, temperature,
                       temperatures_or_null, logp_out, entropy_out_or_null, workspace, workspace_bytes, dstatus,
                       stream, nullptr, 0);
+}
+
+size_t tim_sample_workspace_bytes(int64_t n_tok, int32_t hidden, int32_t vocab) {
+  (void)hidden;
+  if (n_tok < 0 || vocab < 1) return 0;
+  return kWsHeaderBytes + 2u * static_cast<size_t>(vocab_slices(vocab)) * static_cast<size_t>(n_tok) * 16u;
+}
+
+tim_status tim_sample(const void* hidden_bf16, int64_t ld_hidden, const void* weight_bf16, int32_t hidden,
+                      int32_t vocab, const uint64_t* row_keys, int64_t n_tok, uint64_t seed, float temperature,
+                      const float* temperatures_or_null, int64_t* ids_out, float* logp_out,
+                      float* entropy_out_or_null, void* workspace, size_t workspace_bytes,
+                      tim_device_status* dstatus, void* stream) {
+  if (n_tok > 0 && !row_keys) return TIM_ERR_NULL;
+  if (n_tok == 0) row_keys = nullptr;
+  const uint64_t dummy = 0;
+  return logprob_impl(hidden_bf16, ld_hidden, weight_bf16, hidden, vocab, nullptr, n_tok, temperature,
+                      temperatures_or_null, logp_out, entropy_out_or_null, workspace, workspace_bytes, dstatus,
+                      stream, nullptr, 0, n_tok > 0 ? row_keys : &dummy, seed, ids_out);
 }
 
 tim_status tim_stats_finalize(tim_stats* h) {

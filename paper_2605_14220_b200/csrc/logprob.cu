@@ -100,6 +100,55 @@ __device__ __forceinline__ uint64_t make_policy(int kind) {
   return kind == 3 ? policy_evict_last() : kind == 2 ? policy_evict_first() : policy_evict_normal();
 }
 
+// ---------------------------------------------------------------- sampling twin (NEXT-1) --
+// Counter-based Philox4x32-10 (Salmon et al., SC'11): multipliers 0xD2511F53 / 0xCD9E8D57,
+// Weyl key increments 0x9E3779B9 / 0xBB67AE85.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+__device__ __forceinline__ float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Gumbel-max over 32 columns in the log2 domain: score = y - log2(-log2 u) (the Gumbel noise in
+// log2 units up to a constant), u = ((x >> 9) + 1/2) 2^-23 from Philox block (col / 4, 0, key
+// lo, key hi) under the seed.  y = RN(z c) exactly as tim_logprob's gather, so the sampled
+// token's log-prob is bit-identical to tim_logprob's.  Strict '>' in ascending column order:
+// ties go to the lowest column.
+template <bool kTail>
+__device__ __forceinline__ void gumbel_chunk(const uint32_t (&r)[32], float c, int col0, int vocab, uint32_t sk0,
+                                             uint32_t sk1, uint32_t rk_lo, uint32_t rk_hi, float& best_s,
+                                             float& best_y, int& best_col) {
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    const uint4 x = philox4x32_10(make_uint4(static_cast<uint32_t>(col0 >> 2) + g, 0u, rk_lo, rk_hi), sk0, sk1);
+    const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = 4 * g + q;
+      const float u = fmaf(static_cast<float>(xs[q] >> 9), 0x1p-23f, 0x1p-24f);
+      const float y = __uint_as_float(r[i]) * c;
+      float sc = y - lg2_approx(-lg2_approx(u));
+      if (kTail && col0 + i >= vocab) sc = -CUDART_INF_F;
+      if (sc > best_s) {
+        best_s = sc;
+        best_y = y;
+        best_col = col0 + i;
+      }
+    }
+  }
+}
+
 // Static unit schedule (changes only WHICH pair runs a unit, never any row's arithmetic).
 // Pairs form groups of G (G | S_v): in full round r, group q owns M-tile r*ngrp + q and its
 // member g sweeps slices [g S_v/G, (g+1) S_v/G) -- vocab tiles in ascending order, so all pairs
@@ -161,7 +210,7 @@ __device__ __noinline__ uint32_t wait_progress(const uint32_t* prog, uint32_t nc
   return mn;
 }
 
-template <bool kPair, bool kDebug>
+template <bool kPair, bool kDebug, bool kSample>
 __global__ void __launch_bounds__(kThreads, 1)
     logprob_fwd_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constant__ CUtensorMap tmap_w,
                        LogprobParams p) {
@@ -298,10 +347,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int k = 0; sched.unit(cid, k, mt, j); ++k) {
       const int row = mt * C::kUnitM + rank * kCtaM + row_in_cta;
       const bool valid = row < p.n_tok;
-      const int64_t a = valid ? __ldg(p.ids + row) : int64_t(-1);
+      const int64_t a = (valid && p.ids) ? __ldg(p.ids + row) : int64_t(-1);
       const float T = (valid && p.temps) ? __ldg(p.temps + row) : p.temperature;
       const float c = __fdiv_rn(kLog2eF, T);
       float m = -CUDART_INF_F, s = 0.f, uu = 0.f, ya = -CUDART_INF_F;
+      float best_s = -CUDART_INF_F, best_y = -CUDART_INF_F;
+      int best_col = -1;
+      uint32_t rk_lo = 0, rk_hi = 0;
+      if (kSample && valid) {
+        const uint64_t rk = __ldg(reinterpret_cast<const unsigned long long*>(p.row_keys) + row);
+        rk_lo = static_cast<uint32_t>(rk);
+        rk_hi = static_cast<uint32_t>(rk >> 32);
+      }
       const int t0 = (j * p.n_vt) / n_slices, t1 = ((j + 1) * p.n_vt) / n_slices;
       for (int vt = t0; vt < t1; ++vt) {
         if (p.sleep_waits) mbar_wait_sleep(smem_u32(&tfull[acc]), aphase);
@@ -330,11 +387,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             epi_chunk<true>(r, c, col0, p.vocab, a, m, s, uu, ya);
           else
             epi_chunk<false>(r, c, col0, p.vocab, a, m, s, uu, ya);
+          if (kSample) {
+            const uint32_t sk0 = static_cast<uint32_t>(p.seed), sk1 = static_cast<uint32_t>(p.seed >> 32);
+            if (tail_tile)
+              gumbel_chunk<true>(r, c, col0, p.vocab, sk0, sk1, rk_lo, rk_hi, best_s, best_y, best_col);
+            else
+              gumbel_chunk<false>(r, c, col0, p.vocab, sk0, sk1, rk_lo, rk_hi, best_s, best_y, best_col);
+          }
         }
         acc ^= 1;
         if (acc == 0) aphase ^= 1;
       }
-      if (valid) p.partials[static_cast<int64_t>(j) * p.n_tok + row] = make_float4(m, s, uu, ya);
+      if (valid) {
+        p.partials[static_cast<int64_t>(j) * p.n_tok + row] = make_float4(m, s, uu, ya);
+        if (kSample)
+          p.partials2[static_cast<int64_t>(j) * p.n_tok + row] =
+              make_float4(best_s, best_y, __int_as_float(best_col), 0.f);
+      }
     }
   }
 
@@ -378,11 +447,51 @@ __global__ void __launch_bounds__(256) logprob_merge_kernel(MergeParams p) {
   commit_status_last_block(p.ws, p.dstatus);
 }
 
-template <bool kPair, bool kDebug>
+// a4 for the sampling twin: same merge; the sampled column is the best Gumbel score over the
+// slices in slice order (strict '>': ties go to the lowest slice, i.e. the lowest column), and
+// its log-prob uses that column's y exactly as tim_logprob's gather would.
+__global__ void __launch_bounds__(256) sample_merge_kernel(MergeParams p) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < p.n_tok) {
+    double M = -CUDART_INF;
+    for (int j = 0; j < p.n_slices; ++j) M = fmax(M, static_cast<double>(p.partials[j * p.n_tok + t].x));
+    double S = 0.0, U = 0.0;
+    float bs = -CUDART_INF_F, by = -CUDART_INF_F;
+    int bc = -1;
+    for (int j = 0; j < p.n_slices; ++j) {
+      const float4 q = p.partials[j * p.n_tok + t];
+      const double dm = static_cast<double>(q.x) - M;
+      const double w = exp2(dm);
+      S = S + static_cast<double>(q.y) * w;
+      U = U + w * (static_cast<double>(q.z) + static_cast<double>(q.y) * dm);
+      const float4 g = p.partials2[j * p.n_tok + t];
+      if (g.x > bs) {
+        bs = g.x;
+        by = g.y;
+        bc = __float_as_int(g.z);
+      }
+    }
+    bool bad = bc < 0;
+    if (p.temps) {
+      const float T = p.temps[t];
+      bad = bad || !(T > 0.f) || !isfinite(T);
+    }
+    const double l2s = log2(S);
+    const double kLn2 = 0.69314718055994530942;
+    p.ids_out[t] = bad ? -1 : bc;
+    p.logp[t] = bad ? CUDART_NAN_F : static_cast<float>(kLn2 * ((static_cast<double>(by) - M) - l2s));
+    if (p.entropy) p.entropy[t] = static_cast<float>(kLn2 * (l2s - U / S));
+    if (bad) atomicMax(reinterpret_cast<unsigned long long*>(&p.ws->bad_inv),
+                       static_cast<unsigned long long>(kBadSentinel - t));
+  }
+  commit_status_last_block(p.ws, p.dstatus);
+}
+
+template <bool kPair, bool kDebug, bool kSample>
 static cudaError_t launch_fwd(const CUtensorMap& th, const CUtensorMap& tw, const LogprobParams& p, int grid,
                               cudaStream_t stream) {
   using C = KCfg<kPair>;
-  auto kern = logprob_fwd_kernel<kPair, kDebug>;
+  auto kern = logprob_fwd_kernel<kPair, kDebug, kSample>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
@@ -407,10 +516,20 @@ static cudaError_t launch_fwd(const CUtensorMap& th, const CUtensorMap& tw, cons
 int fwd_unit_rows(bool pair) { return pair ? KCfg<true>::kUnitM : KCfg<false>::kUnitM; }
 int fwd_w_box_rows(bool pair) { return pair ? KCfg<true>::kBRows : KCfg<false>::kBRows; }
 
-cudaError_t launch_logprob_fwd(bool pair, bool debug, const CUtensorMap& th, const CUtensorMap& tw,
+cudaError_t launch_logprob_fwd(bool pair, bool debug, bool sample, const CUtensorMap& th, const CUtensorMap& tw,
                                const LogprobParams& p, int grid, cudaStream_t stream) {
-  if (pair) return debug ? launch_fwd<true, true>(th, tw, p, grid, stream) : launch_fwd<true, false>(th, tw, p, grid, stream);
-  return debug ? launch_fwd<false, true>(th, tw, p, grid, stream) : launch_fwd<false, false>(th, tw, p, grid, stream);
+  if (sample) return pair ? launch_fwd<true, false, true>(th, tw, p, grid, stream)
+                          : launch_fwd<false, false, true>(th, tw, p, grid, stream);
+  if (pair) return debug ? launch_fwd<true, true, false>(th, tw, p, grid, stream)
+                         : launch_fwd<true, false, false>(th, tw, p, grid, stream);
+  return debug ? launch_fwd<false, true, false>(th, tw, p, grid, stream)
+               : launch_fwd<false, false, false>(th, tw, p, grid, stream);
+}
+
+cudaError_t launch_sample_merge(const MergeParams& p, cudaStream_t stream) {
+  const int blocks = static_cast<int>((p.n_tok + 255) / 256);
+  sample_merge_kernel<<<blocks, 256, 0, stream>>>(p);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_logprob_merge(const MergeParams& p, cudaStream_t stream) {

@@ -41,6 +41,9 @@ struct LogprobParams {
   uint32_t* progress;   // [clusters] tiles issued per CTA pair (workspace, zeroed per call)
   int sync_slack;       // max tiles a pair may run ahead of the slowest pair (0 = no throttle)
   int group;            // pairs sharing one M-tile (split its slices) so the live H tiles fit in L2
+  const uint64_t* row_keys;  // sampling twin: per-row Philox counter (e.g. sequence << 32 | position)
+  uint64_t seed;             // sampling twin: Philox key
+  float4* partials2;         // sampling twin: {best score, its y, its column, 0} [n_slices][n_tok]
 };
 
 struct MergeParams {
@@ -54,6 +57,8 @@ struct MergeParams {
   int n_slices;
   WsHeader* ws;
   tim_device_status* dstatus;
+  const float4* partials2;  // sampling twin
+  int64_t* ids_out;         // sampling twin
 };
 
 // Commit the call's data-error state to the caller's status word; executed by the last block
@@ -86,9 +91,10 @@ __device__ __forceinline__ void commit_status_last_block(WsHeader* ws, tim_devic
 // logprob.cu
 int fwd_unit_rows(bool pair);
 int fwd_w_box_rows(bool pair);
-cudaError_t launch_logprob_fwd(bool pair, bool debug, const CUtensorMap& th, const CUtensorMap& tw,
+cudaError_t launch_logprob_fwd(bool pair, bool debug, bool sample, const CUtensorMap& th, const CUtensorMap& tw,
                                const LogprobParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_logprob_merge(const MergeParams& p, cudaStream_t stream);
+cudaError_t launch_sample_merge(const MergeParams& p, cudaStream_t stream);
 
 // correct.cu
 struct CorrectDevCfg {

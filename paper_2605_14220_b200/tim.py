@@ -68,6 +68,9 @@ _SIGS = {
     "tim_logprob_workspace_bytes": (_SZ, [_I64, _I32, _I32]),
     "tim_logprob_vocab_slices": (_I32, [_I32]),
     "tim_logprob": (_I32, [_P, _I64, _P, _I32, _I32, _P, _I64, _F, _P, _P, _P, _P, _SZ, _P, _P]),
+    "tim_sample_workspace_bytes": (_SZ, [_I64, _I32, _I32]),
+    "tim_sample": (_I32, [_P, _I64, _P, _I32, _I32, _P, _I64, ctypes.c_uint64, _F, _P, _P, _P, _P, _P, _SZ, _P,
+                          _P]),
     "tim_stats_finalize": (_I32, [_P]),
     "tim_correct_workspace_bytes": (_SZ, [_I64, _I64, _I32]),
     "tim_mismatch_stats": (_I32, [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _SZ, _P, _P]),
@@ -194,6 +197,36 @@ def logprob(hidden: torch.Tensor, weight: torch.Tensor, ids: torch.Tensor, tempe
         lp = lp.to("cpu", non_blocking=False)
         ent = ent.to("cpu") if ent is not None else None
     return lp, ent
+
+
+def sample(hidden: torch.Tensor, weight: torch.Tensor, row_keys: torch.Tensor, seed: int,
+           temperature: float = 1.0, temperatures: torch.Tensor | None = None, entropy: bool = True,
+           status: torch.Tensor | None = None):
+    """Rollout-side twin -- tim_sample: Gumbel-max draw a_t ~ softmax(z_t / T) keyed by (seed,
+    row_keys[t]); returns (ids int64, logp, entropy) with logp / entropy bit-identical to
+    tim_logprob(ids)."""
+    dev = hidden.device
+    if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
+        raise TypeError("hidden and weight must be bfloat16")
+    if hidden.dim() != 2 or hidden.stride(1) != 1:
+        raise ValueError("hidden must be [N, d] with unit inner stride")
+    weight = weight.contiguous()
+    N, d = hidden.shape
+    V = weight.shape[0]
+    row_keys = row_keys.to(device=dev, dtype=torch.int64).contiguous()
+    if row_keys.numel() != N or weight.shape[1] != d:
+        raise ValueError("shape mismatch")
+    if temperatures is not None:
+        temperatures = temperatures.to(device=dev, dtype=torch.float32).contiguous()
+    ids = torch.empty(N, dtype=torch.int64, device=dev)
+    lp = torch.empty(N, dtype=torch.float32, device=dev)
+    ent = torch.empty(N, dtype=torch.float32, device=dev) if entropy else None
+    L = lib()
+    ws = _workspace(dev, L.tim_sample_workspace_bytes(N, d, V), "sample")
+    _check(L.tim_sample(_ptr(hidden), hidden.stride(0), _ptr(weight), d, V, _ptr(row_keys), N,
+                        ctypes.c_uint64(int(seed) % (1 << 64)), float(temperature), _ptr(temperatures), _ptr(ids),
+                        _ptr(lp), _ptr(ent), _ptr(ws), ws.numel(), _ptr(status), _stream(dev)), "tim_sample")
+    return ids, lp, ent
 
 
 def debug_logits(hidden: torch.Tensor, weight: torch.Tensor, ids: torch.Tensor):
