@@ -126,7 +126,7 @@ def run_ours(args):
         vals = [int(x) for x in args.tuning.split(",")]
         tim.debug_set_tuning(*vals[:4])
         if len(vals) > 4:
-            tim.debug_set_group(vals[4])
+            tim.debug_set_schedule(vals[4], vals[5] if len(vals) > 5 else 0)
     if args.max_pairs:
         tim.debug_set_kernel(True, args.max_pairs)
     torch.cuda.set_device(local)
@@ -212,6 +212,28 @@ def run_ours(args):
     if not torch.equal(a.view(torch.int32), ref_bits):
         max_shape_diff = max(max_shape_diff, (a - lp[samp]).abs().max().item())
 
+    # NEXT-1 rollout-side twin on the same batch: draw throughput and the zero-mismatch check
+    sample_info = None
+    if args.sample_bench:
+        keys = (torch.arange(N, device=dev, dtype=torch.int64) << 32) | rank
+        for _ in range(2):
+            sid, slp, sent = tim.sample(H, W, keys, seed=20260001)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            sid, slp, sent = tim.sample(H, W, keys, seed=20260001)
+        e1.record()
+        torch.cuda.synchronize()
+        sms = e0.elapsed_time(e1) / 3
+        rlp, rent = tim.logprob(H, W, sid)
+        same = bool(torch.equal(rlp.view(torch.int32), slp.view(torch.int32)) and
+                    torch.equal(rent.view(torch.int32), sent.view(torch.int32)))
+        sample_info = {"tokens_per_s": N / (sms / 1e3), "ms": sms,
+                       "tflops": 2.0 * cfg.vocab * cfg.hidden * N / (sms / 1e3) / 1e12,
+                       "logp_bitwise_equal_to_logprob": same,
+                       "kernel": "tim_sample (tcgen05 GEMM + online LSE + Philox Gumbel-max epilogue)"}
+
     # end to end through the public API from pinned host buffers
     e2e = None
     Hh = H.cpu().pin_memory()
@@ -286,6 +308,8 @@ def run_ours(args):
         "correction_stats": {k: stats[k] for k in ("n_resp_tok", "n_truncated", "n_seq_rejected", "max_abs_delta",
                                                      "mean_abs_delta", "mean_k3")},
     }
+    if sample_info is not None:
+        out["sample_twin"] = sample_info
     if args.correction_tokens > 0:
         out["correction_roofline"] = correction_roofline(tim, dev, args.correction_tokens, peaks, peak_src)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -442,6 +466,8 @@ def main():
                     help="h_policy,w_policy,sleep,slack[,group] (experiments; results unchanged)")
     ap.add_argument("--max-pairs", type=int, default=0, help="cap the persistent grid (experiments)")
     ap.add_argument("--n-seq", type=int, default=0, help="override the number of sequences (experiments)")
+    ap.add_argument("--no-sample-bench", dest="sample_bench", action="store_false",
+                    help="skip the rollout-side twin (tim_sample) measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -30,10 +30,10 @@ tim_status tim_debug_set_kernel(int32_t use_pair, int32_t max_ctas_or_clusters);
  * sync_slack > 0 bounds how many vocab tiles a CTA pair may run ahead of the slowest pair. */
 tim_status tim_debug_set_tuning(int32_t h_policy, int32_t w_policy, int32_t sleep_waits, int32_t sync_slack);
 
-/* Schedule knob (never changes results): number of CTA pairs sharing one 256-token M-tile
- * (each sweeps S_v/group slices of it); 0 = automatic (smallest group whose live hidden-state
- * tiles fit in ~75% of L2). */
-tim_status tim_debug_set_group(int32_t group);
+/* Schedule knobs (never change results): number of CTA pairs sharing one 256-token M-tile
+ * (each sweeps S_v/group slices of it), 0 = automatic (smallest group whose live hidden-state
+ * tiles fit in ~75% of L2); demote = 1 lowers finished hidden-state tiles to evict_normal in L2. */
+tim_status tim_debug_set_schedule(int32_t group, int32_t demote);
 
 #ifdef __cplusplus
 }

@@ -40,6 +40,7 @@ int g_w_policy = 2;  // W tiles: evict_first (shared by all pairs within a few t
 int g_sleep_waits = 1;
 int g_sync_slack = 4;  // pairs stay within 4 vocab tiles of each other: W window ~4 MB in L2
 int g_group = 0;       // pairs per M-tile group (0 = automatic from the L2 size)
+int g_demote = 0;      // demote finished H tiles to evict_normal (applypriority)
 
 tim_status device_info(DevInfo** out) {
   int dev = 0;
@@ -155,6 +156,9 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   p.sleep_waits = g_sleep_waits;
   p.progress = reinterpret_cast<uint32_t*>(wsb + kWsProgressOffset);
   p.sync_slack = g_sync_slack;
+  p.hidden_ptr = hidden;
+  p.ld_hidden_bytes = ld_hidden * 2;
+  p.demote = g_demote;
   p.row_keys = row_keys;
   p.seed = seed;
   p.partials2 = sample ? partials + static_cast<size_t>(vocab_slices(vocab)) * static_cast<size_t>(n_tok) : nullptr;
@@ -548,9 +552,10 @@ tim_status tim_debug_set_kernel(int32_t use_pair, int32_t max_ctas_or_clusters) 
   return TIM_OK;
 }
 
-tim_status tim_debug_set_group(int32_t group) {
+tim_status tim_debug_set_schedule(int32_t group, int32_t demote) {
   if (group != 0 && group != 1 && group != 2 && group != 4 && group != 8) return TIM_ERR_VALUE;
   g_group = group;
+  g_demote = demote != 0;
   return TIM_OK;
 }
 

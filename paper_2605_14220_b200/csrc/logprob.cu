@@ -177,6 +177,10 @@ struct UnitSched {
     mt = rounds * ngrp + q % rem;
     return true;
   }
+  // unit k is the last one pair c runs on its current M-tile (full rounds only)
+  __device__ __forceinline__ bool last_of_mtile(int c, int k) const {
+    return c < ngrp * G && k < rounds * per_round && (k % per_round) == per_round - 1;
+  }
 };
 
 __device__ __forceinline__ void st_relaxed_gpu(uint32_t* p, uint32_t v) {
@@ -302,6 +306,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
         if (gate && lane == 0) st_relaxed_gpu(p.progress + cid, step + 1);
+      }
+      // This CTA has issued its last load of the M-tile (end of its slice range in a full round):
+      // demote its H rows from evict_last to evict_normal so dead tiles do not crowd W out of L2.
+      if (p.demote && sched.last_of_mtile(cid, k)) {
+        const int rows = min(kCtaM, p.n_tok - m0);
+        const int lines_per_row = p.hidden / 64;  // 128-B lines of one bf16 row
+        const uint8_t* base = static_cast<const uint8_t*>(p.hidden_ptr);
+        for (int e = lane; e < rows * lines_per_row; e += 32) {
+          const int rr = e / lines_per_row, ll = e % lines_per_row;
+          l2_demote(base + static_cast<int64_t>(m0 + rr) * p.ld_hidden_bytes + ll * 128);
+        }
       }
     }
     if (gate && lane == 0) st_relaxed_gpu(p.progress + cid, 0xFFFFFFFFu);

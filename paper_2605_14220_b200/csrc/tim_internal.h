@@ -44,6 +44,9 @@ struct LogprobParams {
   const uint64_t* row_keys;  // sampling twin: per-row Philox counter (e.g. sequence << 32 | position)
   uint64_t seed;             // sampling twin: Philox key
   float4* partials2;         // sampling twin: {best score, its y, its column, 0} [n_slices][n_tok]
+  const void* hidden_ptr;    // H base (for L2 priority demotion of finished M-tiles)
+  int64_t ld_hidden_bytes;
+  int demote;                // demote finished H tiles to evict_normal
 };
 
 struct MergeParams {

@@ -84,7 +84,7 @@ _SIGS = {
     "tim_debug_logprob_logits": (_I32, [_P, _I64, _P, _I32, _I32, _P, _I64, _P, _I64, _P, _P, _P, _SZ, _P]),
     "tim_debug_set_kernel": (_I32, [_I32, _I32]),
     "tim_debug_set_tuning": (_I32, [_I32, _I32, _I32, _I32]),
-    "tim_debug_set_group": (_I32, [_I32]),
+    "tim_debug_set_schedule": (_I32, [_I32, _I32]),
 }
 
 _lib = None
@@ -250,9 +250,9 @@ def debug_set_tuning(h_policy: int = 0, w_policy: int = 0, sleep_waits: bool = F
            "tim_debug_set_tuning")
 
 
-def debug_set_group(group: int = 0):
-    """Schedule knob (results unchanged): CTA pairs per M-tile group, 0 = automatic."""
-    _check(lib().tim_debug_set_group(int(group)), "tim_debug_set_group")
+def debug_set_schedule(group: int = 0, demote: bool = False):
+    """Schedule knobs (results unchanged): CTA pairs per M-tile group (0 = auto), L2 demotion."""
+    _check(lib().tim_debug_set_schedule(int(group), int(demote)), "tim_debug_set_schedule")
 
 
 def debug_set_kernel(use_pair: bool = True, max_ctas: int = 0):
