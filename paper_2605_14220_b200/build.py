@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtim.so")
 SOURCES = ["api.cu", "logprob.cu", "correct.cu"]
-HEADERS = ["ptx.cuh", "tim_internal.h"]
+HEADERS = ["ptx.cuh", "tim_internal.h", "contract.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
