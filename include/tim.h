@@ -258,6 +258,70 @@ tim_status tim_correct_finish(const void* gathered_partials, int32_t nranks,
                               tim_stats* stats_dev_or_null, void* stream);
 
 /* ----------------------------------------------------------------------------
+ * tim_ppo_loss  (fused PPO / GRPO surrogate + loss diagnostics)
+ *
+ * Per token t (PAPER.md eq:ppo_loss P:352-360, eq:ppo_ratio P:361-373, App. A.4):
+ *   r_t   = exp(logp_cur - logp_old)     logp_old = trainer-recomputed (recompute mode) or
+ *                                        rollout log-prob (bypass mode), C.3 exp contract
+ *   clipped_t <=> (A_t > 0 and r_t > clip_hi) or (A_t < 0 and r_t < clip_lo)
+ *   loss_t = -w_t min(r_t A_t, clip(r_t, clip_lo, clip_hi) A_t), w_t = coeff_t (the tim_correct
+ *            coefficient resp * tok_keep * seq_keep * TIS weight) or the response mask
+ *   grad_t = d loss_t / d logp_cur_t = (clipped ? 0 : loss_t)   (score-function gradient)
+ * Diagnostics over contributing tokens (coeff != 0, else response tokens): clip fraction,
+ * K1 / K3 of r, and the zero-centred contribution C(r) = -(r - 1) A
+ * histogrammed separately for A > 0 and A < 0 (A == 0 counted apart).
+ * Aggregation (reading U17): per-sequence loss = sum over its contributing tokens (exact
+ * 2^-52 fixed point, int128), batch_loss = sum of sequence losses / number of sequences with a
+ * contributing token.  Multi-rank: like tim_correct (exact partial blocks, rank-ordered sums).
+ *
+ * Buffers (device): logp_cur, logp_old, advantages [n_tok_local] fp32; coeff_or_null fp32;
+ * resp_mask_or_null u8 (ignored when coeff is given); loss_tok, grad_logp fp32, clipped u8
+ * [n_tok_local]; seq_loss_or_null [n_seq] f64; hist_or_null [2][hist_bins + 2] int64 (slot 0 =
+ * underflow, hist_bins + 1 = overflow; row 0: A > 0, row 1: A < 0); stats optional.
+ * Non-finite logp -> dstatus TIM_ERR_DATA (first global index), that token's loss = NaN.
+ * -------------------------------------------------------------------------- */
+typedef struct {
+  double clip_lo;         /* 1 - eps  (paper eq:ppo_loss) */
+  double clip_hi;         /* 1 + eps                      */
+  double hist_lo;         /* C(r) histogram: lower edge   */
+  double hist_inv_width;  /* hist_bins / (hi - lo)        */
+  int32_t hist_bins;      /* 1 .. 1024                    */
+  int32_t reserved;
+} tim_ppo_cfg;
+
+typedef struct {
+  int64_t n_tok, n_contrib, n_clipped, n_zero_adv, n_saturated;
+  int64_t sum_loss[2], sum_k1[2], sum_k3[2];
+  int64_t reserved[5];
+} tim_ppo_partial_header;  /* 128 B; block = header + hist [2][bins + 2] int64 + n_seq tim_seq_partial */
+
+typedef struct {
+  int64_t n_tok, n_contrib, n_clipped, n_zero_adv, n_saturated, n_seq, n_seq_contrib;
+  int64_t sum_loss_fx[2], sum_k1_fx[2], sum_k3_fx[2];   /* int128 {lo, hi}, scale 2^-52 */
+  double batch_loss, clip_frac, mean_k1, mean_k3;       /* host: tim_ppo_stats_finalize */
+} tim_ppo_stats;
+
+size_t tim_ppo_partial_bytes(int64_t n_seq, int32_t hist_bins);
+size_t tim_ppo_workspace_bytes(int64_t n_seq, int32_t hist_bins, int32_t nranks);
+tim_status tim_ppo_loss(const float* logp_cur, const float* logp_old, const float* advantages,
+                        const float* coeff_or_null, const uint8_t* resp_mask_or_null,
+                        const int64_t* cu_seqlens_global, int64_t n_seq, int64_t tok_begin,
+                        int64_t n_tok_local, const tim_ppo_cfg* cfg_host, tim_comm* comm_or_null,
+                        float* loss_tok, float* grad_logp, uint8_t* clipped,
+                        double* seq_loss_or_null, int64_t* hist_or_null, tim_ppo_stats* stats_dev_or_null,
+                        void* workspace, size_t workspace_bytes, tim_device_status* dstatus, void* stream);
+tim_status tim_ppo_local(const float* logp_cur, const float* logp_old, const float* advantages,
+                         const float* coeff_or_null, const uint8_t* resp_mask_or_null,
+                         const int64_t* cu_seqlens_global, int64_t n_seq, int64_t tok_begin,
+                         int64_t n_tok_local, const tim_ppo_cfg* cfg_host,
+                         float* loss_tok, float* grad_logp, uint8_t* clipped, void* partial_out,
+                         tim_device_status* dstatus, void* stream);
+tim_status tim_ppo_finish(const void* gathered_partials, int32_t nranks, int64_t n_seq,
+                          const tim_ppo_cfg* cfg_host, double* seq_loss_or_null, int64_t* hist_or_null,
+                          tim_ppo_stats* stats_dev_or_null, void* stream);
+tim_status tim_ppo_stats_finalize(tim_ppo_stats* host_copy);
+
+/* ----------------------------------------------------------------------------
  * NCCL communicator (NVLink / NVSwitch).  libnccl.so.2 is loaded at run time.
  * unique_id: 128 bytes from tim_comm_unique_id on rank 0, broadcast by the caller.
  * -------------------------------------------------------------------------- */

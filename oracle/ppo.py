@@ -28,7 +28,7 @@ import dataclasses
 
 import numpy as np
 
-from .correct import _isum, delta, exp_contract, fixed_point, k3_contract
+from .correct import DataError, _isum, delta, exp_contract, fixed_point, k3_contract
 
 
 @dataclasses.dataclass
@@ -45,6 +45,9 @@ def local(lp_cur, lp_old, adv, cu_seqlens, cfg: PPOCfg, coeff=None, resp_mask=No
     S = cu.size - 1
     d = delta(lp_cur, lp_old)
     n = d.size
+    bad = ~np.isfinite(d)
+    if bad.any():
+        raise DataError(tok_begin + int(np.argmax(bad)))
     r = exp_contract(d)
     A = np.asarray(adv, dtype=np.float32).astype(np.float64)
     if coeff is not None:

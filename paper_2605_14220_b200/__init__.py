@@ -6,6 +6,7 @@ marshals torch tensors / streams into that ABI.  There is no CPU fallback: on a 
 the package fails loudly if the library is missing.
 """
 from .tim import (  # noqa: F401
-    CorrectConfig, Comm, TimError, PRESETS, logprob, sample, correct, mismatch_stats, correct_local,
+    CorrectConfig, Comm, TimError, PRESETS, PPOConfig, logprob, sample, correct, mismatch_stats, correct_local,
+    ppo_loss, ppo_local, ppo_finish,
     correct_finish, exchange_partials, lib, library_path, shard_range, vocab_slices,
 )

@@ -95,6 +95,24 @@ bool encode_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t co
 
 inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 
+// int128 {lo, hi} -> double, round to nearest even (bits below 64 significant ones fold into a sticky bit)
+double i128_host_to_double(const int64_t* v) {
+  const __int128 x = (static_cast<__int128>(v[1]) << 64) | static_cast<__int128>(static_cast<uint64_t>(v[0]));
+  const bool neg = x < 0;
+  const unsigned __int128 u = neg ? static_cast<unsigned __int128>(-x) : static_cast<unsigned __int128>(x);
+  const uint64_t hi = static_cast<uint64_t>(u >> 64);
+  double r;
+  if (hi == 0) {
+    r = static_cast<double>(static_cast<uint64_t>(u));  // RN (default rounding mode)
+  } else {
+    const int sh = 64 - __builtin_clzll(hi);
+    uint64_t top = static_cast<uint64_t>(u >> sh);
+    if ((u & ((static_cast<unsigned __int128>(1) << sh) - 1)) != 0) top |= 1u;
+    r = std::ldexp(static_cast<double>(top), sh);
+  }
+  return neg ? -r : r;
+}
+
 constexpr int kMaxSlices = 8;
 inline int32_t n_vocab_tiles(int32_t vocab) { return (vocab + 255) / 256; }
 inline int32_t vocab_slices(int32_t vocab) {
@@ -530,6 +548,131 @@ tim_status tim_comm_destroy(tim_comm* comm) {
   NcclApi* api = nccl();
   if (api->ok && comm->comm) api->destroy(comm->comm);
   delete comm;
+  return TIM_OK;
+}
+
+// ------------------------------------------------------------------ PPO (NEXT-2) --
+static tim_status check_ppo_cfg(const tim_ppo_cfg* c) {
+  if (!c) return TIM_ERR_NULL;
+  if (!std::isfinite(c->clip_lo) || !std::isfinite(c->clip_hi) || !(c->clip_lo <= c->clip_hi)) return TIM_ERR_VALUE;
+  if (!std::isfinite(c->hist_lo) || !std::isfinite(c->hist_inv_width) || !(c->hist_inv_width > 0.0))
+    return TIM_ERR_VALUE;
+  if (c->hist_bins < 1 || c->hist_bins > ppo_max_hist_bins()) return TIM_ERR_VALUE;
+  return TIM_OK;
+}
+
+size_t tim_ppo_partial_bytes(int64_t n_seq, int32_t hist_bins) {
+  if (n_seq < 0 || hist_bins < 1) return 0;
+  return sizeof(tim_ppo_partial_header) + 16u * static_cast<size_t>(hist_bins + 2) +
+         static_cast<size_t>(n_seq) * sizeof(tim_seq_partial);
+}
+
+size_t tim_ppo_workspace_bytes(int64_t n_seq, int32_t hist_bins, int32_t nranks) {
+  if (n_seq < 0 || hist_bins < 1 || nranks < 1) return 0;
+  const size_t b = (tim_ppo_partial_bytes(n_seq, hist_bins) + 255) & ~size_t(255);
+  return b * (1 + static_cast<size_t>(nranks));
+}
+
+tim_status tim_ppo_local(const float* cur, const float* old, const float* adv, const float* coeff, const uint8_t* resp,
+                         const int64_t* cu, int64_t n_seq, int64_t tok_begin, int64_t n_local, const tim_ppo_cfg* cfg,
+                         float* loss, float* grad, uint8_t* clipped, void* partial_out, tim_device_status* dstatus,
+                         void* stream) {
+  tim_status st = check_common(cur, old, cu, n_seq, tok_begin, n_local, resp);
+  if (st != TIM_OK) return st;
+  if ((st = check_ppo_cfg(cfg)) != TIM_OK) return st;
+  if (!partial_out) return TIM_ERR_NULL;
+  if (n_local > 0 && (!adv || !loss || !grad || !clipped)) return TIM_ERR_NULL;
+  if (!aligned(partial_out, 16)) return TIM_ERR_ALIGN;
+  DevInfo* dev = nullptr;
+  if ((st = device_info(&dev)) != TIM_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(partial_out, 0, tim_ppo_partial_bytes(n_seq, cfg->hist_bins), s) != cudaSuccess)
+    return TIM_ERR_CUDA;
+  if (n_local == 0) return TIM_OK;
+  PpoLocalParams p{};
+  p.cur = cur;
+  p.old = old;
+  p.adv = adv;
+  p.coeff = coeff;
+  p.resp = resp;
+  p.cu = cu;
+  p.n_seq = n_seq;
+  p.tok_begin = tok_begin;
+  p.n = n_local;
+  p.clip_lo = cfg->clip_lo;
+  p.clip_hi = cfg->clip_hi;
+  p.hist_lo = cfg->hist_lo;
+  p.hist_inv_width = cfg->hist_inv_width;
+  p.bins = cfg->hist_bins;
+  p.loss = loss;
+  p.grad = grad;
+  p.clipped = clipped;
+  uint8_t* blk = static_cast<uint8_t*>(partial_out);
+  p.hdr = reinterpret_cast<tim_ppo_partial_header*>(blk);
+  p.hist = reinterpret_cast<int64_t*>(blk + sizeof(tim_ppo_partial_header));
+  p.seqp = reinterpret_cast<tim_seq_partial*>(blk + sizeof(tim_ppo_partial_header) +
+                                              16u * static_cast<size_t>(cfg->hist_bins + 2));
+  p.dstatus = dstatus;
+  return launch_ppo_local(p, dev->num_sms, s) == cudaSuccess ? TIM_OK : TIM_ERR_CUDA;
+}
+
+tim_status tim_ppo_finish(const void* gathered, int32_t nranks, int64_t n_seq, const tim_ppo_cfg* cfg,
+                          double* seq_loss, int64_t* hist, tim_ppo_stats* stats, void* stream) {
+  if (!gathered) return TIM_ERR_NULL;
+  if (nranks < 1 || n_seq < 0) return TIM_ERR_SHAPE;
+  tim_status st = check_ppo_cfg(cfg);
+  if (st != TIM_OK) return st;
+  if (!aligned(gathered, 16)) return TIM_ERR_ALIGN;
+  DevInfo* dev = nullptr;
+  if ((st = device_info(&dev)) != TIM_OK) return st;
+  PpoFinishParams f{};
+  f.gathered = static_cast<const uint8_t*>(gathered);
+  f.block_bytes = static_cast<int64_t>(tim_ppo_partial_bytes(n_seq, cfg->hist_bins));
+  f.nranks = nranks;
+  f.n_seq = n_seq;
+  f.bins = cfg->hist_bins;
+  f.seq_loss = seq_loss;
+  f.hist = hist;
+  f.stats = stats;
+  return launch_ppo_finish(f, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? TIM_OK : TIM_ERR_CUDA;
+}
+
+tim_status tim_ppo_loss(const float* cur, const float* old, const float* adv, const float* coeff, const uint8_t* resp,
+                        const int64_t* cu, int64_t n_seq, int64_t tok_begin, int64_t n_local, const tim_ppo_cfg* cfg,
+                        tim_comm* comm, float* loss, float* grad, uint8_t* clipped, double* seq_loss, int64_t* hist,
+                        tim_ppo_stats* stats, void* ws, size_t ws_bytes, tim_device_status* dstatus, void* stream) {
+  tim_status st = check_ppo_cfg(cfg);
+  if (st != TIM_OK) return st;
+  const int nranks = comm ? comm->nranks : 1;
+  if (!ws) return TIM_ERR_NULL;
+  if (!aligned(ws, 256)) return TIM_ERR_ALIGN;
+  if (ws_bytes < tim_ppo_workspace_bytes(n_seq, cfg->hist_bins, nranks)) return TIM_ERR_WORKSPACE;
+  uint8_t* local = static_cast<uint8_t*>(ws);
+  const size_t blk = (tim_ppo_partial_bytes(n_seq, cfg->hist_bins) + 255) & ~size_t(255);
+  if ((st = tim_ppo_local(cur, old, adv, coeff, resp, cu, n_seq, tok_begin, n_local, cfg, loss, grad, clipped, local,
+                          dstatus, stream)) != TIM_OK)
+    return st;
+  const void* gathered = local;
+  if (comm != nullptr) {
+    NcclApi* api = nccl();
+    if (!api->ok) return TIM_ERR_NCCL;
+    if (api->all_gather(local, local + blk, tim_ppo_partial_bytes(n_seq, cfg->hist_bins), kNcclInt8, comm->comm,
+                        reinterpret_cast<cudaStream_t>(stream)) != 0)
+      return TIM_ERR_NCCL;
+    gathered = local + blk;
+  }
+  return tim_ppo_finish(gathered, nranks, n_seq, cfg, seq_loss, hist, stats, stream);
+}
+
+tim_status tim_ppo_stats_finalize(tim_ppo_stats* h) {
+  if (!h) return TIM_ERR_NULL;
+  const double sc = std::ldexp(1.0, -52);
+  const double nc = static_cast<double>(h->n_contrib);
+  h->batch_loss = h->n_seq_contrib ? (i128_host_to_double(h->sum_loss_fx) * sc) / static_cast<double>(h->n_seq_contrib)
+                                   : 0.0;
+  h->clip_frac = h->n_contrib ? static_cast<double>(h->n_clipped) / nc : 0.0;
+  h->mean_k1 = h->n_contrib ? (i128_host_to_double(h->sum_k1_fx) * sc) / nc : 0.0;
+  h->mean_k3 = h->n_contrib ? (i128_host_to_double(h->sum_k3_fx) * sc) / nc : 0.0;
   return TIM_OK;
 }
 

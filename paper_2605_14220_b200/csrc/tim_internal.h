@@ -138,6 +138,41 @@ struct ZeroParams {
   const uint8_t* seq_keep;
   float* coeff;
 };
+// ppo.cu
+struct PpoLocalParams {
+  const float* cur;
+  const float* old;
+  const float* adv;
+  const float* coeff;    // may be null (then resp / all)
+  const uint8_t* resp;   // may be null
+  const int64_t* cu;
+  int64_t n_seq;
+  int64_t tok_begin;
+  int64_t n;
+  double clip_lo, clip_hi, hist_lo, hist_inv_width;
+  int bins;
+  float* loss;
+  float* grad;
+  uint8_t* clipped;
+  tim_ppo_partial_header* hdr;
+  int64_t* hist;         // [2][bins + 2] inside the partial block
+  tim_seq_partial* seqp;
+  tim_device_status* dstatus;
+};
+struct PpoFinishParams {
+  const uint8_t* gathered;
+  int64_t block_bytes;
+  int nranks;
+  int64_t n_seq;
+  int bins;
+  double* seq_loss;      // may be null
+  int64_t* hist;         // may be null
+  tim_ppo_stats* stats;  // may be null
+};
+int ppo_max_hist_bins();
+cudaError_t launch_ppo_local(const PpoLocalParams& p, int num_sms, cudaStream_t stream);
+cudaError_t launch_ppo_finish(const PpoFinishParams& p, cudaStream_t stream);
+
 cudaError_t launch_correct_local(const LocalParams& p, int num_sms, cudaStream_t stream);
 cudaError_t launch_correct_finish(const FinishParams& p, cudaStream_t stream);
 cudaError_t launch_correct_zero(const ZeroParams& p, cudaStream_t stream);

@@ -78,6 +78,13 @@ _SIGS = {
     "tim_correct_partial_bytes": (_SZ, [_I64]),
     "tim_correct_local": (_I32, [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "tim_correct_finish": (_I32, [_P, _I32, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P]),
+    "tim_ppo_partial_bytes": (_SZ, [_I64, _I32]),
+    "tim_ppo_workspace_bytes": (_SZ, [_I64, _I32, _I32]),
+    "tim_ppo_loss": (_I32, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P,
+                            _P]),
+    "tim_ppo_local": (_I32, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P]),
+    "tim_ppo_finish": (_I32, [_P, _I32, _I64, _P, _P, _P, _P, _P]),
+    "tim_ppo_stats_finalize": (_I32, [_P]),
     "tim_comm_unique_id": (_I32, [_P]),
     "tim_comm_init": (_I32, [_P, _I32, _I32, ctypes.POINTER(_P)]),
     "tim_comm_destroy": (_I32, [_P]),
@@ -376,6 +383,116 @@ def mismatch_stats(lp_num, lp_den, cu_seqlens, resp_mask=None, tok_begin: int = 
                                 comm.handle if comm is not None else None, _ptr(raw), _ptr(ws), ws.numel(),
                                 _ptr(status), _stream(dev)), "tim_mismatch_stats")
     return stats_from_bytes(raw)
+
+
+# ------------------------------------------------------------------------------ PPO (NEXT-2) --
+class PpoCfgC(ctypes.Structure):
+    _fields_ = [("clip_lo", ctypes.c_double), ("clip_hi", ctypes.c_double), ("hist_lo", ctypes.c_double),
+                ("hist_inv_width", ctypes.c_double), ("hist_bins", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class PpoStatsC(ctypes.Structure):
+    _fields_ = [("n_tok", ctypes.c_int64), ("n_contrib", ctypes.c_int64), ("n_clipped", ctypes.c_int64),
+                ("n_zero_adv", ctypes.c_int64), ("n_saturated", ctypes.c_int64), ("n_seq", ctypes.c_int64),
+                ("n_seq_contrib", ctypes.c_int64), ("sum_loss_fx", ctypes.c_int64 * 2),
+                ("sum_k1_fx", ctypes.c_int64 * 2), ("sum_k3_fx", ctypes.c_int64 * 2), ("batch_loss", ctypes.c_double),
+                ("clip_frac", ctypes.c_double), ("mean_k1", ctypes.c_double), ("mean_k3", ctypes.c_double)]
+
+
+PPO_STATS_BYTES = ctypes.sizeof(PpoStatsC)
+
+
+@dataclasses.dataclass
+class PPOConfig:
+    """tim_ppo_cfg: clip(r, 1 - eps, 1 + eps) (eq:ppo_loss) and the C(r) histogram range."""
+
+    eps: float = 0.2
+    hist_lo: float = -1.0
+    hist_hi: float = 1.0
+    hist_bins: int = 64
+
+    def to_c(self) -> PpoCfgC:
+        return PpoCfgC(1.0 - self.eps, 1.0 + self.eps, float(self.hist_lo),
+                       self.hist_bins / (self.hist_hi - self.hist_lo), int(self.hist_bins), 0)
+
+
+def ppo_stats_from_bytes(raw: torch.Tensor) -> dict:
+    st = PpoStatsC.from_buffer_copy(bytes(raw.cpu().numpy().tobytes()))
+    _check(lib().tim_ppo_stats_finalize(ctypes.byref(st)), "tim_ppo_stats_finalize")
+
+    def i128(a):
+        return int(a[0]) % (1 << 64) + (int(a[1]) << 64)
+
+    return {"n_tok": st.n_tok, "n_contrib": st.n_contrib, "n_clipped": st.n_clipped, "n_zero_adv": st.n_zero_adv,
+            "n_saturated": st.n_saturated, "n_seq": st.n_seq, "n_seq_contrib": st.n_seq_contrib,
+            "sum_loss": i128(st.sum_loss_fx), "sum_k1": i128(st.sum_k1_fx), "sum_k3": i128(st.sum_k3_fx),
+            "batch_loss": st.batch_loss, "clip_frac": st.clip_frac, "mean_k1": st.mean_k1, "mean_k3": st.mean_k3}
+
+
+def ppo_loss(lp_cur: torch.Tensor, lp_old: torch.Tensor, advantages: torch.Tensor, cu_seqlens: torch.Tensor,
+             cfg: PPOConfig, coeff: torch.Tensor | None = None, resp_mask: torch.Tensor | None = None,
+             tok_begin: int = 0, comm: "Comm | None" = None, status: torch.Tensor | None = None,
+             return_stats: bool = True):
+    """Fused clipped surrogate + diagnostics -- tim_ppo_loss (device tensors)."""
+    dev = lp_cur.device
+    _, lp_cur, lp_old, cu_seqlens, resp_mask = _prep_correct(lp_cur, lp_old, cu_seqlens, resp_mask, dev)
+    adv = advantages.to(device=dev, dtype=torch.float32).contiguous()
+    if coeff is not None:
+        coeff = coeff.to(device=dev, dtype=torch.float32).contiguous()
+    n = lp_cur.numel()
+    S = cu_seqlens.numel() - 1
+    nranks = comm.nranks if comm is not None else 1
+    c = cfg.to_c()
+    out = {"loss": torch.empty(n, dtype=torch.float32, device=dev),
+           "grad": torch.empty(n, dtype=torch.float32, device=dev),
+           "clipped": torch.empty(n, dtype=torch.uint8, device=dev),
+           "seq_loss": torch.empty(S, dtype=torch.float64, device=dev),
+           "hist": torch.empty(2, cfg.hist_bins + 2, dtype=torch.int64, device=dev),
+           "stats_raw": torch.zeros(PPO_STATS_BYTES, dtype=torch.uint8, device=dev)}
+    L = lib()
+    ws = _workspace(dev, L.tim_ppo_workspace_bytes(S, cfg.hist_bins, nranks), "ppo")
+    _check(L.tim_ppo_loss(_ptr(lp_cur), _ptr(lp_old), _ptr(adv), _ptr(coeff), _ptr(resp_mask), _ptr(cu_seqlens), S,
+                          int(tok_begin), n, ctypes.byref(c), comm.handle if comm is not None else None,
+                          _ptr(out["loss"]), _ptr(out["grad"]), _ptr(out["clipped"]), _ptr(out["seq_loss"]),
+                          _ptr(out["hist"]), _ptr(out["stats_raw"]), _ptr(ws), ws.numel(), _ptr(status),
+                          _stream(dev)), "tim_ppo_loss")
+    if return_stats:
+        out["stats"] = ppo_stats_from_bytes(out["stats_raw"])
+    return out
+
+
+def ppo_local(lp_cur, lp_old, advantages, cu_seqlens, cfg: PPOConfig, coeff=None, resp_mask=None,
+              tok_begin: int = 0, status=None):
+    """Split form, pass 1 of tim_ppo_loss: per-token outputs + this rank's exact partial block."""
+    dev = lp_cur.device
+    _, lp_cur, lp_old, cu_seqlens, resp_mask = _prep_correct(lp_cur, lp_old, cu_seqlens, resp_mask, dev)
+    adv = advantages.to(device=dev, dtype=torch.float32).contiguous()
+    if coeff is not None:
+        coeff = coeff.to(device=dev, dtype=torch.float32).contiguous()
+    n = lp_cur.numel()
+    S = cu_seqlens.numel() - 1
+    c = cfg.to_c()
+    out = {"loss": torch.empty(n, dtype=torch.float32, device=dev),
+           "grad": torch.empty(n, dtype=torch.float32, device=dev),
+           "clipped": torch.empty(n, dtype=torch.uint8, device=dev),
+           "partial": torch.empty(int(lib().tim_ppo_partial_bytes(S, cfg.hist_bins)), dtype=torch.uint8, device=dev)}
+    _check(lib().tim_ppo_local(_ptr(lp_cur), _ptr(lp_old), _ptr(adv), _ptr(coeff), _ptr(resp_mask), _ptr(cu_seqlens),
+                               S, int(tok_begin), n, ctypes.byref(c), _ptr(out["loss"]), _ptr(out["grad"]),
+                               _ptr(out["clipped"]), _ptr(out["partial"]), _ptr(status), _stream(dev)),
+           "tim_ppo_local")
+    return out
+
+
+def ppo_finish(gathered: torch.Tensor, nranks: int, n_seq: int, cfg: PPOConfig):
+    """Split form, pass 2: exact rank-ordered combine -> sequence losses, histogram, stats."""
+    dev = gathered.device
+    c = cfg.to_c()
+    out = {"seq_loss": torch.empty(n_seq, dtype=torch.float64, device=dev),
+           "hist": torch.empty(2, cfg.hist_bins + 2, dtype=torch.int64, device=dev),
+           "stats_raw": torch.zeros(PPO_STATS_BYTES, dtype=torch.uint8, device=dev)}
+    _check(lib().tim_ppo_finish(_ptr(gathered), int(nranks), int(n_seq), ctypes.byref(c), _ptr(out["seq_loss"]),
+                                _ptr(out["hist"]), _ptr(out["stats_raw"]), _stream(dev)), "tim_ppo_finish")
+    return out
 
 
 def partial_bytes(n_seq: int) -> int:
