@@ -312,6 +312,7 @@ def run_ours(args):
         out["sample_twin"] = sample_info
     if args.correction_tokens > 0:
         out["correction_roofline"] = correction_roofline(tim, dev, args.correction_tokens, peaks, peak_src)
+        out["ppo_roofline"] = ppo_roofline(tim, dev, args.correction_tokens, peaks, peak_src)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"], out["max_abs_dlogp_vs_oracle"] = cpu_baseline(cfg, W, Hh, ids, lp, lp_roll, mask,
                                                                             args.cpu_seconds)
@@ -325,6 +326,33 @@ def run_ours(args):
 
 def H_bytes(cfg):
     return cfg.n_tok * cfg.hidden * 2
+
+
+def ppo_roofline(tim, dev, n, peaks, peak_src, reps=10):
+    """Standalone tim_ppo_loss (NEXT-2) at n tokens weighted by correction coefficients: 25
+    algorithmic bytes per token (read lp_cur, lp_old, advantage, coeff; write loss, grad, clip flag)."""
+    S = n // 4096
+    cu = synth.cu_seqlens(S, 4096).to(dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(20260005)
+    old = -torch.empty(n, device=dev).exponential_(0.7, generator=g)
+    cur = synth.policy_move(old, 20260005, sd=0.05)
+    adv = torch.randn(n, device=dev, generator=g)
+    coeff = torch.where(torch.arange(n, device=dev) % 4096 >= 1024, 1.0, 0.0).float()
+    cfg = tim.PPOConfig(eps=0.2)
+    for _ in range(3):
+        tim.ppo_loss(cur, old, adv, cu, cfg, coeff=coeff, return_stats=False)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in evs:
+        a.record()
+        tim.ppo_loss(cur, old, adv, cu, cfg, coeff=coeff, return_stats=False)
+        b.record()
+    torch.cuda.synchronize()
+    ms = sorted(a.elapsed_time(b) for a, b in evs)[reps // 2]
+    gbs = 25.0 * n / (ms / 1e3) / 1e9
+    peak = float(peaks["hbm_gbs"])
+    return {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak, "n_tok": n, "ms": ms,
+            "algorithmic_bytes_per_token": 25, "kernel": "tim_ppo_loss (ppo_local + finish, median of %d)" % reps}
 
 
 def correction_roofline(tim, dev, n, peaks, peak_src, reps=10):

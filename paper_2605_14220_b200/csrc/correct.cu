@@ -23,12 +23,18 @@
 
 namespace tim {
 
-constexpr int kTpl = 8;                 // tokens per lane
+#ifndef TIM_CORR_TPL
+#define TIM_CORR_TPL 4
+#endif
+#ifndef TIM_CORR_MINB
+#define TIM_CORR_MINB 3
+#endif
+constexpr int kTpl = TIM_CORR_TPL;      // tokens per lane
 constexpr int kWarpTok = 32 * kTpl;     // tokens per warp chunk
 constexpr int kLocalThreads = 256;
 
 template <bool kOut, bool kSeq>
-__global__ void __launch_bounds__(kLocalThreads, 2) correct_local_kernel(LocalParams p) {
+__global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_kernel(LocalParams p) {
   const int lane = threadIdx.x & 31;
   const long long warp_g = (static_cast<long long>(blockIdx.x) * kLocalThreads + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * kLocalThreads) >> 5;
@@ -60,21 +66,22 @@ __global__ void __launch_bounds__(kLocalThreads, 2) correct_local_kernel(LocalPa
     const long long i0 = ch * kWarpTok + lane * kTpl;
     float num[kTpl], den[kTpl];
     uint8_t rs[kTpl];
-    const bool full = i0 + kTpl <= p.n;
+    const bool full = (kTpl % 4 == 0) && i0 + kTpl <= p.n;  // vector path needs whole float4s
     if (full) {
-      const float4* pn = reinterpret_cast<const float4*>(p.num + i0);
-      const float4* pd = reinterpret_cast<const float4*>(p.den + i0);
-      const float4 n0 = __ldg(pn), n1 = __ldg(pn + 1), d0 = __ldg(pd), d1 = __ldg(pd + 1);
-      num[0] = n0.x; num[1] = n0.y; num[2] = n0.z; num[3] = n0.w;
-      num[4] = n1.x; num[5] = n1.y; num[6] = n1.z; num[7] = n1.w;
-      den[0] = d0.x; den[1] = d0.y; den[2] = d0.z; den[3] = d0.w;
-      den[4] = d1.x; den[5] = d1.y; den[6] = d1.z; den[7] = d1.w;
+#pragma unroll
+      for (int v = 0; v < kTpl / 4; ++v) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(p.num + i0) + v);
+        const float4 b = __ldg(reinterpret_cast<const float4*>(p.den + i0) + v);
+        num[4 * v] = a.x; num[4 * v + 1] = a.y; num[4 * v + 2] = a.z; num[4 * v + 3] = a.w;
+        den[4 * v] = b.x; den[4 * v + 1] = b.y; den[4 * v + 2] = b.z; den[4 * v + 3] = b.w;
+      }
       if (p.resp) {
-        const uint2 m = __ldg(reinterpret_cast<const uint2*>(p.resp + i0));
 #pragma unroll
-        for (int k = 0; k < 4; ++k) rs[k] = (m.x >> (8 * k)) & 0xff;
+        for (int v = 0; v < kTpl / 4; ++v) {
+          const uint32_t m = __ldg(reinterpret_cast<const uint32_t*>(p.resp + i0) + v);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) rs[4 + k] = (m.y >> (8 * k)) & 0xff;
+          for (int k = 0; k < 4; ++k) rs[4 * v + k] = (m >> (8 * k)) & 0xff;
+        }
       } else {
 #pragma unroll
         for (int k = 0; k < kTpl; ++k) rs[k] = 1;
@@ -154,12 +161,13 @@ __global__ void __launch_bounds__(kLocalThreads, 2) correct_local_kernel(LocalPa
       k_out[k] = keep ? 1 : 0;
       c_out[k] = (resp && keep) ? w_out[k] : 0.f;
 
-      bool sat_abs, sat1, sat3;
+      bool sat1, sat3;
       const long long x1 = fixed_point(-d, sat1);
       const double k3 = k3v[k];
       const long long x3 = fixed_point(k3, sat3);
       if (resp) {
-        const long long xa = fixed_point(fabs(d), sat_abs);
+        // rint is odd-symmetric and |K1| = |delta| saturate together: X(|delta|) = |X(-delta)|
+        const long long xa = x1 < 0 ? -x1 : x1;
         c_resp += 1;
         c_trunc += trunc ? 1 : 0;
         c_rej += keep ? 0 : 1;
@@ -192,14 +200,14 @@ __global__ void __launch_bounds__(kLocalThreads, 2) correct_local_kernel(LocalPa
       if (full) {
         float4* pw = reinterpret_cast<float4*>(p.tis_w + i0);
         float4* pc = reinterpret_cast<float4*>(p.coeff + i0);
-        pw[0] = make_float4(w_out[0], w_out[1], w_out[2], w_out[3]);
-        pw[1] = make_float4(w_out[4], w_out[5], w_out[6], w_out[7]);
-        pc[0] = make_float4(c_out[0], c_out[1], c_out[2], c_out[3]);
-        pc[1] = make_float4(c_out[4], c_out[5], c_out[6], c_out[7]);
-        uint2 kk;
-        kk.x = k_out[0] | (k_out[1] << 8) | (k_out[2] << 16) | (static_cast<uint32_t>(k_out[3]) << 24);
-        kk.y = k_out[4] | (k_out[5] << 8) | (k_out[6] << 16) | (static_cast<uint32_t>(k_out[7]) << 24);
-        *reinterpret_cast<uint2*>(p.tok_keep + i0) = kk;
+#pragma unroll
+        for (int v = 0; v < kTpl / 4; ++v) {
+          pw[v] = make_float4(w_out[4 * v], w_out[4 * v + 1], w_out[4 * v + 2], w_out[4 * v + 3]);
+          pc[v] = make_float4(c_out[4 * v], c_out[4 * v + 1], c_out[4 * v + 2], c_out[4 * v + 3]);
+          reinterpret_cast<uint32_t*>(p.tok_keep + i0)[v] =
+              k_out[4 * v] | (k_out[4 * v + 1] << 8) | (k_out[4 * v + 2] << 16) |
+              (static_cast<uint32_t>(k_out[4 * v + 3]) << 24);
+        }
       } else {
 #pragma unroll
         for (int k = 0; k < kTpl; ++k) {
@@ -381,7 +389,7 @@ cudaError_t launch_correct_local(const LocalParams& p, int num_sms, cudaStream_t
   const long long chunks = (p.n + kWarpTok - 1) / kWarpTok;
   const long long warps_per_block = kLocalThreads / 32;
   long long blocks = (chunks + warps_per_block - 1) / warps_per_block;
-  const long long cap = static_cast<long long>(num_sms) * 2;  // one resident wave (2 blocks / SM)
+  const long long cap = static_cast<long long>(num_sms) * TIM_CORR_MINB;  // one resident wave
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   const bool out = p.tis_w != nullptr;

@@ -21,7 +21,7 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libtim.so")
+_LIB_PATH = os.environ.get("TIM_LIBRARY") or os.path.join(_HERE, "libtim.so")  # override: A/B builds
 
 TIM_OK = 0
 _STATUS = {0: "TIM_OK", 1: "TIM_ERR_NULL", 2: "TIM_ERR_SHAPE", 3: "TIM_ERR_ALIGN", 4: "TIM_ERR_VALUE",
