@@ -129,6 +129,8 @@ def run_ours(args):
             tim.debug_set_schedule(vals[4], vals[5] if len(vals) > 5 else 0)
     if args.max_pairs:
         tim.debug_set_kernel(True, args.max_pairs)
+    if args.cluster_pairs:
+        tim.debug_set_cluster(args.cluster_pairs)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -494,6 +496,7 @@ def main():
                     help="h_policy,w_policy,sleep,slack[,group] (experiments; results unchanged)")
     ap.add_argument("--max-pairs", type=int, default=0, help="cap the persistent grid (experiments)")
     ap.add_argument("--n-seq", type=int, default=0, help="override the number of sequences (experiments)")
+    ap.add_argument("--cluster-pairs", type=int, default=0, help="1 or 2 CTA pairs per cluster (experiments)")
     ap.add_argument("--no-sample-bench", dest="sample_bench", action="store_false",
                     help="skip the rollout-side twin (tim_sample) measurement")
     args = ap.parse_args()

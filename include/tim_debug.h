@@ -35,6 +35,11 @@ tim_status tim_debug_set_tuning(int32_t h_policy, int32_t w_policy, int32_t slee
  * tiles fit in ~75% of L2); demote = 1 lowers finished hidden-state tiles to evict_normal in L2. */
 tim_status tim_debug_set_schedule(int32_t group, int32_t demote);
 
+/* Cluster shape knob (never changes results): 1 = clusters of one CTA pair; 2 = clusters of two
+ * pairs that own different M-tiles and share every W tile through TMA multicast (used only when
+ * the live hidden-state tiles of all pairs fit in L2). */
+tim_status tim_debug_set_cluster(int32_t pairs_per_cluster);
+
 #ifdef __cplusplus
 }
 #endif

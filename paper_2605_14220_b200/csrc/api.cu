@@ -41,6 +41,7 @@ int g_sleep_waits = 1;
 int g_sync_slack = 4;  // pairs stay within 4 vocab tiles of each other: W window ~4 MB in L2
 int g_group = 0;       // pairs per M-tile group (0 = automatic from the L2 size)
 int g_demote = 0;      // demote finished H tiles to evict_normal (applypriority)
+int g_quad = 0;        // 2-pair clusters sharing W tiles through TMA multicast
 
 tim_status device_info(DevInfo** out) {
   int dev = 0;
@@ -145,9 +146,14 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   if (st != TIM_OK) return st;
 
   const bool pair = g_use_pair != 0;
+  // 2-pair multicast clusters when the live H tiles of all pairs fit in L2 (d <= 2048 on B200);
+  // otherwise 1-pair clusters with M-tile groups (below).  Never changes a result bit.
+  const bool quad = pair && g_quad != 0 && dev->max_pair_clusters >= 2 &&
+                    dev->max_pair_clusters * 256.0 * d * 2.0 <= 0.75 * dev->l2_bytes;
   CUtensorMap th, tw;
   if (!encode_bf16_2d(&th, hidden, n_tok, d, ld_hidden, 128)) return TIM_ERR_CUDA;
-  if (!encode_bf16_2d(&tw, weight, vocab, d, d, fwd_w_box_rows(pair))) return TIM_ERR_CUDA;
+  if (!encode_bf16_2d(&tw, weight, vocab, d, d, quad ? fwd_w_box_rows(pair) / 2 : fwd_w_box_rows(pair)))
+    return TIM_ERR_CUDA;
 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   uint8_t* wsb = static_cast<uint8_t*>(ws);
@@ -180,16 +186,18 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   p.row_keys = row_keys;
   p.seed = seed;
   p.partials2 = sample ? partials + static_cast<size_t>(vocab_slices(vocab)) * static_cast<size_t>(n_tok) : nullptr;
-  const int64_t n_units = static_cast<int64_t>(p.n_mt) * p.n_slices;
-  int64_t ctas_cap = pair ? dev->max_pair_clusters : dev->max_single_ctas;
+  const int64_t n_units = static_cast<int64_t>(quad ? (p.n_mt + 1) / 2 : p.n_mt) * p.n_slices;
+  int64_t ctas_cap = quad ? dev->max_pair_clusters / 2 : (pair ? dev->max_pair_clusters : dev->max_single_ctas);
   if (g_max_clusters > 0 && g_max_clusters < ctas_cap) ctas_cap = g_max_clusters;
   const int64_t groups = n_units < ctas_cap ? n_units : ctas_cap;
-  const int grid = static_cast<int>(groups * (pair ? 2 : 1));
+  const int grid = static_cast<int>(groups * (quad ? 4 : (pair ? 2 : 1)));
   // Pairs sharing an M-tile: smallest G in {1, 2, 4, 8} (dividing S_v, <= #pairs) whose live H
   // tiles (one 256-row tile per group) fit in ~75% of L2.  Performance only: which pair runs
   // which (M-tile, slice) unit never changes a row's arithmetic.
   p.group = 1;
-  if (pair && g_group > 0) {
+  if (quad) {
+    p.group = 1;
+  } else if (pair && g_group > 0) {
     if (p.n_slices % g_group == 0 && groups >= g_group) p.group = g_group;
   } else if (pair) {
     const double h_tile = 256.0 * d * 2.0;
@@ -197,7 +205,7 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
            (static_cast<double>(groups) / p.group) * h_tile > 0.75 * dev->l2_bytes)
       p.group *= 2;
   }
-  if (launch_logprob_fwd(pair, debug_logits != nullptr, sample, th, tw, p, grid, s) != cudaSuccess)
+  if (launch_logprob_fwd(pair, debug_logits != nullptr, sample, quad, th, tw, p, grid, s) != cudaSuccess)
     return TIM_ERR_CUDA;
 
   MergeParams mp{};
@@ -692,6 +700,12 @@ tim_status tim_debug_set_kernel(int32_t use_pair, int32_t max_ctas_or_clusters) 
   if (max_ctas_or_clusters < 0) return TIM_ERR_VALUE;
   g_use_pair = use_pair;
   g_max_clusters = max_ctas_or_clusters;
+  return TIM_OK;
+}
+
+tim_status tim_debug_set_cluster(int32_t pairs_per_cluster) {
+  if (pairs_per_cluster != 1 && pairs_per_cluster != 2) return TIM_ERR_VALUE;
+  g_quad = pairs_per_cluster == 2;
   return TIM_OK;
 }
 

@@ -214,11 +214,14 @@ __device__ __noinline__ uint32_t wait_progress(const uint32_t* prog, uint32_t nc
   return mn;
 }
 
-template <bool kPair, bool kDebug, bool kSample>
+// kNP = CTA pairs per cluster: 1 (cluster of 2) or 2 (cluster of 4: the two pairs own different
+// M-tiles, sweep the same vocab tiles in lock-step and share every W tile through TMA multicast).
+template <bool kPair, bool kDebug, bool kSample, int kNP>
 __global__ void __launch_bounds__(kThreads, 1)
     logprob_fwd_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constant__ CUtensorMap tmap_w,
                        LogprobParams p) {
   using C = KCfg<kPair>;
+  static_assert(kNP == 1 || (kPair && kNP == 2), "multicast clusters are built from CTA pairs");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
@@ -233,14 +236,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = kPair ? cluster_ctarank() : 0u;
-  const bool leader = rank == 0;
+  const uint32_t prank = rank & 1u;      // rank inside the CTA pair
+  const uint32_t pid = rank >> 1;        // pair inside the cluster
+  const uint32_t pl = rank & ~1u;        // rank of this pair's leader CTA
+  const bool leader = prank == 0;
   const uint32_t cid = kPair ? cluster_id_x() : blockIdx.x;
   const uint32_t ncl = kPair ? ncluster_x() : gridDim.x;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), 1);
+      mbar_init(smem_u32(&empty[s]), kNP);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(&tfull[a]), 1);
@@ -260,25 +266,32 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int n_slices = p.n_slices;
   const int nkb = p.hidden / kBlockK;
-  const UnitSched sched(p.n_mt, n_slices, ncl, p.group);
+  const UnitSched sched((p.n_mt + kNP - 1) / kNP, n_slices, ncl, p.group);
 
   if (warp == 0) {
     // ===================== TMA producer (whole warp; lane 0 issues) =====================
     uint32_t stage = 0, phase = 0;
     const uint64_t pol_h = make_policy(p.h_policy), pol_w = make_policy(p.w_policy);
     const bool hints = p.h_policy != 0 || p.w_policy != 0;
-    const bool gate = kPair && leader && p.sync_slack > 0 && p.progress != nullptr;
+    const bool publish = kPair && rank == 0 && p.sync_slack > 0 && p.progress != nullptr;
+    bool gate = publish;
     uint32_t step = 0, known_min = 0;
-    int mt, j;
-    for (int k = 0; sched.unit(cid, k, mt, j); ++k) {
-      const int m0 = mt * C::kUnitM + rank * kCtaM;
+    int dm, j;
+    for (int k = 0; sched.unit(cid, k, dm, j); ++k) {
+      const int mt = dm * kNP + pid;
+      const int m0 = mt * C::kUnitM + prank * kCtaM;
       const int t0 = (j * p.n_vt) / n_slices, t1 = ((j + 1) * p.n_vt) / n_slices;
       for (int vt = t0; vt < t1; ++vt, ++step) {
         // bound the drift between pairs sweeping the same W tiles (performance only:
         // the wait is time-limited, results never depend on it)
-        if (gate && static_cast<uint64_t>(step) > static_cast<uint64_t>(known_min) + p.sync_slack)
+        if (gate && static_cast<uint64_t>(step) > static_cast<uint64_t>(known_min) + p.sync_slack) {
           known_min = wait_progress(p.progress, ncl, step - p.sync_slack, lane);
-        const int n0 = vt * kTileN + rank * C::kBRows;
+          // a pair that never shows up (not co-resident: another kernel holds SMs, or a cluster
+          // shape the GPU cannot place everywhere) must not throttle us: stop gating after a
+          // timed-out wait
+          if (known_min + p.sync_slack < step) gate = false;
+        }
+        const int n0 = vt * kTileN + prank * C::kBRows + (kNP == 2 ? pid * (C::kBRows / 2) : 0);
         for (int kb = 0; kb < nkb; ++kb) {
           if (p.sleep_waits) mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
           else mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
@@ -286,7 +299,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t fb_local = smem_u32(&full[stage]);
             const uint32_t a_dst = smem_u32(smem_a + stage * C::kABytes);
             const uint32_t b_dst = smem_u32(smem_b + stage * C::kBBytes);
-            if (kPair) {
+            if (kNP == 2) {
+              // own H rows -> own smem; half of the W half-tile this CTA and its counterpart in the
+              // other pair both need -> multicast into both.  Bytes land on each destination's
+              // pair-leader barrier (peer bit cleared), 64 KB per pair per stage as before.
+              if (leader) mbar_arrive_expect_tx(fb_local, 2 * C::kStageBytes);
+              const uint32_t fb_pair = fb_local & 0xFEFFFFFFu;
+              const uint16_t mc = static_cast<uint16_t>((1u << prank) | (1u << (prank + 2)));
+              tma_load_2d_pair_hint(a_dst, &tmap_h, mapa(fb_local, pl), kb * kBlockK, m0, pol_h);
+              tma_load_2d_pair_mc_hint(b_dst + pid * (C::kBBytes / 2), &tmap_w, fb_pair, mc, kb * kBlockK, n0,
+                                       pol_w);
+            } else if (kPair) {
               if (leader) mbar_arrive_expect_tx(fb_local, 2 * C::kStageBytes);
               const uint32_t fb = mapa(fb_local, 0);
               if (hints) {
@@ -305,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
-        if (gate && lane == 0) st_relaxed_gpu(p.progress + cid, step + 1);
+        if (publish && lane == 0) st_relaxed_gpu(p.progress + cid, step + 1);
       }
       // This CTA has issued its last load of the M-tile (end of its slice range in a full round):
       // demote its H rows from evict_last to evict_normal so dead tiles do not crowd W out of L2.
@@ -319,15 +342,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    if (gate && lane == 0) st_relaxed_gpu(p.progress + cid, 0xFFFFFFFFu);
+    if (publish && lane == 0) st_relaxed_gpu(p.progress + cid, 0xFFFFFFFFu);
   } else if (warp == 1) {
     // ===================== MMA issuer (one thread of the leader CTA) =====================
     if (leader && lane == 0) {
       const uint32_t idesc = umma_idesc_bf16_f32(kPair ? 256 : 128, kTileN);
-      const uint16_t mask = kPair ? 0x3 : 0x1;
+      const uint16_t mask_empty = kNP == 2 ? 0xF : (kPair ? 0x3 : 0x1);
+      const uint16_t mask_full = static_cast<uint16_t>((kPair ? 0x3 : 0x1) << pl);
       uint32_t stage = 0, phase = 0, acc = 0, aphase = 0;
-      int mt, j;
-      for (int k = 0; sched.unit(cid, k, mt, j); ++k) {
+      int dm, j;
+      for (int k = 0; sched.unit(cid, k, dm, j); ++k) {
         const int t0 = (j * p.n_vt) / n_slices, t1 = ((j + 1) * p.n_vt) / n_slices;
         for (int vt = t0; vt < t1; ++vt) {
           mbar_wait(smem_u32(&tempty[acc]), aphase ^ 1);
@@ -343,10 +367,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               umma_bf16<C::kCtaGroup>(d_tmem, umma_desc_sw128(a0 + kk * kUmmaK * 2),
                                       umma_desc_sw128(b0 + kk * kUmmaK * 2), idesc, (kb | kk) != 0);
             }
-            umma_commit_mc<C::kCtaGroup>(smem_u32(&empty[stage]), mask);
+            umma_commit_mc<C::kCtaGroup>(smem_u32(&empty[stage]), mask_empty);
             if (++stage == C::kStages) { stage = 0; phase ^= 1; }
           }
-          umma_commit_mc<C::kCtaGroup>(smem_u32(&tfull[acc]), mask);
+          umma_commit_mc<C::kCtaGroup>(smem_u32(&tfull[acc]), mask_full);
           acc ^= 1;
           if (acc == 0) aphase ^= 1;
         }
@@ -356,11 +380,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================== epilogue warps: TMEM -> registers -> online LSE =====================
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int row_in_cta = q * 32 + lane;
-    const uint32_t tempty_leader = kPair ? mapa(smem_u32(tempty), 0) : smem_u32(tempty);
+    const uint32_t tempty_leader = kPair ? mapa(smem_u32(tempty), pl) : smem_u32(tempty);
     uint32_t acc = 0, aphase = 0;
-    int mt, j;
-    for (int k = 0; sched.unit(cid, k, mt, j); ++k) {
-      const int row = mt * C::kUnitM + rank * kCtaM + row_in_cta;
+    int dm, j;
+    for (int k = 0; sched.unit(cid, k, dm, j); ++k) {
+      const int mt = dm * kNP + pid;
+      const int row = mt * C::kUnitM + prank * kCtaM + row_in_cta;
       const bool valid = row < p.n_tok;
       const int64_t a = (valid && p.ids) ? __ldg(p.ids + row) : int64_t(-1);
       const float T = (valid && p.temps) ? __ldg(p.temps + row) : p.temperature;
@@ -502,11 +527,11 @@ __global__ void __launch_bounds__(256) sample_merge_kernel(MergeParams p) {
   commit_status_last_block(p.ws, p.dstatus);
 }
 
-template <bool kPair, bool kDebug, bool kSample>
+template <bool kPair, bool kDebug, bool kSample, int kNP>
 static cudaError_t launch_fwd(const CUtensorMap& th, const CUtensorMap& tw, const LogprobParams& p, int grid,
                               cudaStream_t stream) {
   using C = KCfg<kPair>;
-  auto kern = logprob_fwd_kernel<kPair, kDebug, kSample>;
+  auto kern = logprob_fwd_kernel<kPair, kDebug, kSample, kNP>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
@@ -520,7 +545,7 @@ static cudaError_t launch_fwd(const CUtensorMap& th, const CUtensorMap& tw, cons
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kPair ? 2 : 1;
+  attr[0].val.clusterDim.x = kPair ? 2 * kNP : 1;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -531,14 +556,17 @@ static cudaError_t launch_fwd(const CUtensorMap& th, const CUtensorMap& tw, cons
 int fwd_unit_rows(bool pair) { return pair ? KCfg<true>::kUnitM : KCfg<false>::kUnitM; }
 int fwd_w_box_rows(bool pair) { return pair ? KCfg<true>::kBRows : KCfg<false>::kBRows; }
 
-cudaError_t launch_logprob_fwd(bool pair, bool debug, bool sample, const CUtensorMap& th, const CUtensorMap& tw,
-                               const LogprobParams& p, int grid, cudaStream_t stream) {
-  if (sample) return pair ? launch_fwd<true, false, true>(th, tw, p, grid, stream)
-                          : launch_fwd<false, false, true>(th, tw, p, grid, stream);
-  if (pair) return debug ? launch_fwd<true, true, false>(th, tw, p, grid, stream)
-                         : launch_fwd<true, false, false>(th, tw, p, grid, stream);
-  return debug ? launch_fwd<false, true, false>(th, tw, p, grid, stream)
-               : launch_fwd<false, false, false>(th, tw, p, grid, stream);
+cudaError_t launch_logprob_fwd(bool pair, bool debug, bool sample, bool quad, const CUtensorMap& th,
+                               const CUtensorMap& tw, const LogprobParams& p, int grid, cudaStream_t stream) {
+  if (quad) return sample ? launch_fwd<true, false, true, 2>(th, tw, p, grid, stream)
+                          : (debug ? launch_fwd<true, true, false, 2>(th, tw, p, grid, stream)
+                                   : launch_fwd<true, false, false, 2>(th, tw, p, grid, stream));
+  if (sample) return pair ? launch_fwd<true, false, true, 1>(th, tw, p, grid, stream)
+                          : launch_fwd<false, false, true, 1>(th, tw, p, grid, stream);
+  if (pair) return debug ? launch_fwd<true, true, false, 1>(th, tw, p, grid, stream)
+                         : launch_fwd<true, false, false, 1>(th, tw, p, grid, stream);
+  return debug ? launch_fwd<false, true, false, 1>(th, tw, p, grid, stream)
+               : launch_fwd<false, false, false, 1>(th, tw, p, grid, stream);
 }
 
 cudaError_t launch_sample_merge(const MergeParams& p, cudaStream_t stream) {

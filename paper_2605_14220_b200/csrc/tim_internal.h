@@ -94,8 +94,8 @@ __device__ __forceinline__ void commit_status_last_block(WsHeader* ws, tim_devic
 // logprob.cu
 int fwd_unit_rows(bool pair);
 int fwd_w_box_rows(bool pair);
-cudaError_t launch_logprob_fwd(bool pair, bool debug, bool sample, const CUtensorMap& th, const CUtensorMap& tw,
-                               const LogprobParams& p, int grid, cudaStream_t stream);
+cudaError_t launch_logprob_fwd(bool pair, bool debug, bool sample, bool quad, const CUtensorMap& th,
+                               const CUtensorMap& tw, const LogprobParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_logprob_merge(const MergeParams& p, cudaStream_t stream);
 cudaError_t launch_sample_merge(const MergeParams& p, cudaStream_t stream);
 

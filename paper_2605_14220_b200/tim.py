@@ -92,6 +92,7 @@ _SIGS = {
     "tim_debug_set_kernel": (_I32, [_I32, _I32]),
     "tim_debug_set_tuning": (_I32, [_I32, _I32, _I32, _I32]),
     "tim_debug_set_schedule": (_I32, [_I32, _I32]),
+    "tim_debug_set_cluster": (_I32, [_I32]),
 }
 
 _lib = None
@@ -260,6 +261,11 @@ def debug_set_tuning(h_policy: int = 0, w_policy: int = 0, sleep_waits: bool = F
 def debug_set_schedule(group: int = 0, demote: bool = False):
     """Schedule knobs (results unchanged): CTA pairs per M-tile group (0 = auto), L2 demotion."""
     _check(lib().tim_debug_set_schedule(int(group), int(demote)), "tim_debug_set_schedule")
+
+
+def debug_set_cluster(pairs_per_cluster: int = 1):
+    """Cluster shape knob (results unchanged): 2 = two CTA pairs sharing W through TMA multicast."""
+    _check(lib().tim_debug_set_cluster(int(pairs_per_cluster)), "tim_debug_set_cluster")
 
 
 def debug_set_kernel(use_pair: bool = True, max_ctas: int = 0):

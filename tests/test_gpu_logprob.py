@@ -201,3 +201,24 @@ def test_full_c1_batch_sampled_parity_and_invariance(tim):
         a, b = tim.logprob(H[r:r + 1], W, ids[r:r + 1])
         assert _bits(a)[0] == _bits(lp)[r] and _bits(b)[0] == _bits(ent)[r]
     assert torch.isfinite(lp).all() and torch.isfinite(ent).all()
+
+
+@pytest.mark.parametrize("N,d,V", [(300, 256, 1000), (1, 64, 300), (2048, 2048, 151936), (1100, 512, 5000)])
+def test_multicast_cluster_variant_is_bitwise_identical(tim, N, d, V):
+    """Clusters of two CTA pairs sharing W through TMA multicast (performance variant) must give
+    the same bits as single-pair clusters, and the right raw accumulators."""
+    from paper_2605_14220_b200.tim import debug_logits, debug_set_cluster
+    H, W, ids = _case(N, d, V, 90 + N, "peaked")
+    ref = tim.logprob(H, W, ids)
+    try:
+        debug_set_cluster(2)
+        got = tim.logprob(H, W, ids)
+        if V <= 5000:
+            z, _, _ = debug_logits(H, W, ids)
+            torch.cuda.synchronize()
+            refz = oracle_logits(H.cpu(), W.cpu())
+            bound = (H.cpu().double().abs() @ W.cpu().double().abs().T).numpy() * (d * 2.0 ** -23) + 1e-6
+            assert np.all(np.abs(z.cpu().double().numpy() - refz) <= bound)
+    finally:
+        debug_set_cluster(1)
+    assert torch.equal(_bits(got[0]), _bits(ref[0])) and torch.equal(_bits(got[1]), _bits(ref[1]))
