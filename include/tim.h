@@ -258,6 +258,31 @@ tim_status tim_correct_finish(const void* gathered_partials, int32_t nranks,
                               tim_stats* stats_dev_or_null, void* stream);
 
 /* ----------------------------------------------------------------------------
+ * tim_rmsnorm / tim_logprob_rmsnorm  (the batch-invariant RMSNorm
+ * prologue of the head, §3.1)
+ *
+ * Hugging Face Qwen3 RMSNorm semantics (the paper's models):
+ *   x1[t,k]  = bf16( h[t,k] * 1/sqrt(mean_k h[t,k]^2 + eps) )    (fp32, IEEE sqrt / div)
+ *   out[t,k] = bf16( gamma[k] * x1[t,k] )
+ * The sum of squares of a row is reduced in an order fixed by `hidden` only (batch-invariant).
+ *   hidden_bf16 [n_tok, hidden] row pitch ld_hidden (16-B aligned, ld_hidden % 8 == 0);
+ *   gamma_bf16 [hidden]; out_bf16 [n_tok, hidden] contiguous; hidden % 64 == 0; eps >= 0.
+ * tim_logprob_rmsnorm = tim_rmsnorm into the workspace followed by tim_logprob on the
+ * normalized rows (the same outputs and errors as tim_logprob);
+ * workspace >= tim_logprob_rmsnorm_workspace_bytes(n_tok, hidden, vocab).
+ * -------------------------------------------------------------------------- */
+tim_status tim_rmsnorm(const void* hidden_bf16, int64_t ld_hidden, const void* gamma_bf16, float eps,
+                       int32_t hidden, int64_t n_tok, void* out_bf16, void* stream);
+size_t tim_logprob_rmsnorm_workspace_bytes(int64_t n_tok, int32_t hidden, int32_t vocab);
+tim_status tim_logprob_rmsnorm(const void* hidden_bf16, int64_t ld_hidden, const void* gamma_bf16, float eps,
+                               const void* weight_bf16, int32_t hidden, int32_t vocab,
+                               const int64_t* token_ids, int64_t n_tok,
+                               float temperature, const float* temperatures_or_null,
+                               float* logp_out, float* entropy_out_or_null,
+                               void* workspace, size_t workspace_bytes,
+                               tim_device_status* dstatus, void* stream);
+
+/* ----------------------------------------------------------------------------
  * tim_ppo_loss  (fused PPO / GRPO surrogate + loss diagnostics)
  *
  * Per token t (PAPER.md eq:ppo_loss P:352-360, eq:ppo_ratio P:361-373, App. A.4):

@@ -559,6 +559,49 @@ tim_status tim_comm_destroy(tim_comm* comm) {
   return TIM_OK;
 }
 
+// --------------------------------------------------------------- RMSNorm (NEXT-4) --
+tim_status tim_rmsnorm(const void* hidden, int64_t ld_hidden, const void* gamma, float eps, int32_t d, int64_t n_tok,
+                       void* out, void* stream) {
+  if (n_tok < 0 || d < 64 || d > 16384 || d % 64 != 0 || ld_hidden < d) return TIM_ERR_SHAPE;
+  if (!(eps >= 0.f) || !std::isfinite(eps)) return TIM_ERR_VALUE;
+  if (n_tok == 0) return TIM_OK;
+  if (!hidden || !gamma || !out) return TIM_ERR_NULL;
+  if (!aligned(hidden, 16) || !aligned(gamma, 16) || !aligned(out, 16) || ld_hidden % 8 != 0) return TIM_ERR_ALIGN;
+  DevInfo* dev = nullptr;
+  tim_status st = device_info(&dev);
+  if (st != TIM_OK) return st;
+  RmsNormParams p{};
+  p.h = static_cast<const uint16_t*>(hidden);
+  p.ld = ld_hidden;
+  p.gamma = static_cast<const uint16_t*>(gamma);
+  p.eps = eps;
+  p.d = d;
+  p.n = n_tok;
+  p.out = static_cast<uint16_t*>(out);
+  return launch_rmsnorm(p, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? TIM_OK : TIM_ERR_CUDA;
+}
+
+size_t tim_logprob_rmsnorm_workspace_bytes(int64_t n_tok, int32_t hidden, int32_t vocab) {
+  if (n_tok < 0 || hidden < 1 || vocab < 1) return 0;
+  const size_t x = (static_cast<size_t>(n_tok) * static_cast<size_t>(hidden) * 2u + 255) & ~size_t(255);
+  return x + tim_logprob_workspace_bytes(n_tok, hidden, vocab);
+}
+
+tim_status tim_logprob_rmsnorm(const void* hidden, int64_t ld_hidden, const void* gamma, float eps, const void* weight,
+                               int32_t d, int32_t vocab, const int64_t* ids, int64_t n_tok, float temperature,
+                               const float* temps, float* logp, float* ent, void* ws, size_t ws_bytes,
+                               tim_device_status* dstatus, void* stream) {
+  if (n_tok > 0 && !ws) return TIM_ERR_NULL;
+  if (n_tok > 0 && !aligned(ws, 256)) return TIM_ERR_ALIGN;
+  if (n_tok > 0 && ws_bytes < tim_logprob_rmsnorm_workspace_bytes(n_tok, d, vocab)) return TIM_ERR_WORKSPACE;
+  const size_t xb = (static_cast<size_t>(n_tok) * static_cast<size_t>(d) * 2u + 255) & ~size_t(255);
+  void* x = ws;
+  tim_status st = tim_rmsnorm(hidden, ld_hidden, gamma, eps, d, n_tok, x, stream);
+  if (st != TIM_OK) return st;
+  return tim_logprob(n_tok ? x : nullptr, d, weight, d, vocab, ids, n_tok, temperature, temps, logp, ent,
+                     n_tok ? static_cast<uint8_t*>(ws) + xb : nullptr, n_tok ? ws_bytes - xb : 0, dstatus, stream);
+}
+
 // ------------------------------------------------------------------ PPO (NEXT-2) --
 static tim_status check_ppo_cfg(const tim_ppo_cfg* c) {
   if (!c) return TIM_ERR_NULL;

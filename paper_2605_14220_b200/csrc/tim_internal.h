@@ -170,6 +170,18 @@ struct PpoFinishParams {
   tim_ppo_stats* stats;  // may be null
 };
 int ppo_max_hist_bins();
+
+// rmsnorm.cu
+struct RmsNormParams {
+  const uint16_t* h;      // bf16 [n][ld] (pre-norm hidden states)
+  int64_t ld;
+  const uint16_t* gamma;  // bf16 [d]
+  float eps;
+  int d;
+  int64_t n;
+  uint16_t* out;          // bf16 [n][d]
+};
+cudaError_t launch_rmsnorm(const RmsNormParams& p, cudaStream_t stream);
 cudaError_t launch_ppo_local(const PpoLocalParams& p, int num_sms, cudaStream_t stream);
 cudaError_t launch_ppo_finish(const PpoFinishParams& p, cudaStream_t stream);
 

@@ -78,6 +78,9 @@ _SIGS = {
     "tim_correct_partial_bytes": (_SZ, [_I64]),
     "tim_correct_local": (_I32, [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "tim_correct_finish": (_I32, [_P, _I32, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P]),
+    "tim_rmsnorm": (_I32, [_P, _I64, _P, _F, _I32, _I64, _P, _P]),
+    "tim_logprob_rmsnorm_workspace_bytes": (_SZ, [_I64, _I32, _I32]),
+    "tim_logprob_rmsnorm": (_I32, [_P, _I64, _P, _F, _P, _I32, _I32, _P, _I64, _F, _P, _P, _P, _P, _SZ, _P, _P]),
     "tim_ppo_partial_bytes": (_SZ, [_I64, _I32]),
     "tim_ppo_workspace_bytes": (_SZ, [_I64, _I32, _I32]),
     "tim_ppo_loss": (_I32, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P,
@@ -235,6 +238,38 @@ def sample(hidden: torch.Tensor, weight: torch.Tensor, row_keys: torch.Tensor, s
                         ctypes.c_uint64(int(seed) % (1 << 64)), float(temperature), _ptr(temperatures), _ptr(ids),
                         _ptr(lp), _ptr(ent), _ptr(ws), ws.numel(), _ptr(status), _stream(dev)), "tim_sample")
     return ids, lp, ent
+
+
+def rmsnorm(hidden: torch.Tensor, gamma: torch.Tensor, eps: float = 1e-6) -> torch.Tensor:
+    """Batch-invariant RMSNorm (HF Qwen3 semantics, bf16 in / out) -- tim_rmsnorm."""
+    N, d = hidden.shape
+    out = torch.empty(N, d, dtype=torch.bfloat16, device=hidden.device)
+    gamma = gamma.to(device=hidden.device, dtype=torch.bfloat16).contiguous()
+    _check(lib().tim_rmsnorm(_ptr(hidden), hidden.stride(0), _ptr(gamma), float(eps), d, N, _ptr(out),
+                             _stream(hidden.device)), "tim_rmsnorm")
+    return out
+
+
+def logprob_rmsnorm(hidden: torch.Tensor, gamma: torch.Tensor, weight: torch.Tensor, ids: torch.Tensor,
+                    eps: float = 1e-6, temperature: float = 1.0, temperatures: torch.Tensor | None = None,
+                    status: torch.Tensor | None = None):
+    """RMSNorm prologue + log-prob / entropy of the normalized rows -- tim_logprob_rmsnorm."""
+    dev = hidden.device
+    N, d = hidden.shape
+    V = weight.shape[0]
+    gamma = gamma.to(device=dev, dtype=torch.bfloat16).contiguous()
+    weight = weight.contiguous()
+    ids = ids.to(device=dev, dtype=torch.int64).contiguous()
+    if temperatures is not None:
+        temperatures = temperatures.to(device=dev, dtype=torch.float32).contiguous()
+    lp = torch.empty(N, dtype=torch.float32, device=dev)
+    ent = torch.empty(N, dtype=torch.float32, device=dev)
+    L = lib()
+    ws = _workspace(dev, L.tim_logprob_rmsnorm_workspace_bytes(N, d, V), "logprob_rmsnorm")
+    _check(L.tim_logprob_rmsnorm(_ptr(hidden), hidden.stride(0), _ptr(gamma), float(eps), _ptr(weight), d, V,
+                                 _ptr(ids), N, float(temperature), _ptr(temperatures), _ptr(lp), _ptr(ent), _ptr(ws),
+                                 ws.numel(), _ptr(status), _stream(dev)), "tim_logprob_rmsnorm")
+    return lp, ent
 
 
 def debug_logits(hidden: torch.Tensor, weight: torch.Tensor, ids: torch.Tensor):
