@@ -1,0 +1,23 @@
+"""Small invocations of every kernel for compute-sanitizer (memcheck / racecheck / synccheck)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import synth
+from paper_2605_14220_b200 import tim
+
+dev = torch.device("cuda")
+cfg = synth.CONFIGS["toy"]
+W = synth.head_weight(1000, 256, 1, device=dev)
+ids = synth.token_ids(300, 1000, 1, device=dev)
+H = synth.hidden_states(300, 256, 1, device=dev, weight=W, ids=ids, mode="peaked")
+lp, ent = tim.logprob(H, W, ids)
+sid, slp, sent = tim.sample(H, W, torch.arange(300, device=dev), seed=5)
+g = torch.ones(256, dtype=torch.bfloat16, device=dev)
+x = tim.rmsnorm(H, g)
+cu = synth.cu_seqlens(3, 100).to(dev)
+mask = synth.resp_mask(cu.cpu(), 10).to(dev)
+roll = synth.perturb_laplace_mix(lp, 3)
+res = tim.correct(lp, roll, cu, tim.PRESETS["tis-srs-k3-corr-ratio"], mask)
+pp = tim.ppo_loss(lp, roll, torch.randn(300, device=dev), cu, tim.PPOConfig(), coeff=res["coeff"])
+torch.cuda.synchronize()
+print("sanitize run ok", float(lp.sum()), res["stats"]["n_seq_rejected"], pp["stats"]["n_clipped"])
