@@ -174,6 +174,8 @@ def logprob(hidden: torch.Tensor, weight: torch.Tensor, ids: torch.Tensor, tempe
     """
     host = not hidden.is_cuda
     dev = torch.device(device) if device is not None else (hidden.device if not host else torch.device("cuda"))
+    if host and out is None and hidden.shape[0] >= 2 * _HOST_CHUNK:
+        return _logprob_from_host(hidden, weight, ids, temperature, temperatures, entropy, status, dev)
     if host:
         hidden = hidden.to(dev, non_blocking=True)
         ids = ids.to(dev, non_blocking=True)
@@ -208,6 +210,43 @@ def logprob(hidden: torch.Tensor, weight: torch.Tensor, ids: torch.Tensor, tempe
         lp = lp.to("cpu", non_blocking=False)
         ent = ent.to("cpu") if ent is not None else None
     return lp, ent
+
+
+_HOST_CHUNK = 65536          # rows per host->device chunk (a multiple of the 256-row pair tile)
+_copy_streams: dict = {}
+
+
+def _logprob_from_host(hidden, weight, ids, temperature, temperatures, entropy, status, dev):
+    """Host inputs: the H2D copy of chunk i + 1 (copy stream) overlaps tim_logprob on chunk i
+    (caller's stream).  Rows are independent and the kernel is batch-invariant, so the chunked
+    result is bit-identical to one call on the whole batch."""
+    N, d = hidden.shape
+    if not weight.is_cuda:
+        weight = weight.to(dev, non_blocking=True)
+    weight = weight.contiguous()
+    cs = _copy_streams.get(str(dev))
+    if cs is None:
+        cs = _copy_streams[str(dev)] = torch.cuda.Stream(dev)
+    comp = torch.cuda.current_stream(dev)
+    hd = torch.empty(N, d, dtype=torch.bfloat16, device=dev)
+    ids_d = ids.to(dev, non_blocking=True).to(torch.int64)
+    temps_d = temperatures.to(dev, non_blocking=True) if temperatures is not None else None
+    cuts = list(range(0, N, _HOST_CHUNK)) + [N]
+    evs = []
+    cs.wait_stream(comp)
+    with torch.cuda.stream(cs):
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            hd[a:b].copy_(hidden[a:b], non_blocking=True)
+            e = torch.cuda.Event()
+            e.record(cs)
+            evs.append(e)
+    lp = torch.empty(N, dtype=torch.float32, device=dev)
+    ent = torch.empty(N, dtype=torch.float32, device=dev) if entropy else None
+    for (a, b), e in zip(zip(cuts[:-1], cuts[1:]), evs):
+        comp.wait_event(e)
+        logprob(hd[a:b], weight, ids_d[a:b], temperature, temps_d[a:b] if temps_d is not None else None,
+                entropy, out=(lp[a:b], ent[a:b] if ent is not None else None), status=status)
+    return lp.cpu(), (ent.cpu() if ent is not None else None)
 
 
 def sample(hidden: torch.Tensor, weight: torch.Tensor, row_keys: torch.Tensor, seed: int,

@@ -222,3 +222,15 @@ def test_multicast_cluster_variant_is_bitwise_identical(tim, N, d, V):
     finally:
         debug_set_cluster(1)
     assert torch.equal(_bits(got[0]), _bits(ref[0])) and torch.equal(_bits(got[1]), _bits(ref[1]))
+
+
+def test_host_inputs_pipelined_path_is_bitwise_identical(tim):
+    """Host (pinned) inputs take the chunked path whose H2D copies overlap the kernel; the
+    result must equal the device-resident call bit for bit."""
+    N, d, V = 3 * 65536 + 1000, 256, 1000
+    H, W, ids = _case(N, d, V, 95)
+    ref = tim.logprob(H, W, ids)
+    Hh = H.cpu().pin_memory()
+    lp, ent = tim.logprob(Hh, W, ids.cpu(), device=DEV)
+    assert not lp.is_cuda
+    assert torch.equal(lp.view(torch.int32), _bits(ref[0])) and torch.equal(ent.view(torch.int32), _bits(ref[1]))
