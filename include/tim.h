@@ -258,6 +258,33 @@ tim_status tim_correct_finish(const void* gathered_partials, int32_t nranks,
                               tim_stats* stats_dev_or_null, void* stream);
 
 /* ----------------------------------------------------------------------------
+ * Vocab-parallel (tensor-parallel) head  (§5 P:651 TBIK:
+ * reductions invariant to the TP degree)
+ *
+ * The fixed vocab split of tim_logprob (S_v slices, U20) doubles as the TP split: with tp | S_v,
+ * rank r owns slices [r S_v/tp, (r+1) S_v/tp) = W rows [begin, end) from tim_tp_vocab_range.
+ * tim_logprob_tp_partial runs those slices against the rank's shard weight_shard[end - begin, hidden]
+ * and writes (S_v/tp) x n_tok slice partials (16 B each, slice-major) to partial_out
+ * (tim_logprob_tp_partial_bytes).  All-gather the blocks of all ranks contiguously in rank order
+ * (that is the full [S_v][n_tok] slice-major array) and call tim_logprob_tp_merge: logp / entropy
+ * are BIT-IDENTICAL to tim_logprob on the unsharded weight, for every tp -- the cross-rank
+ * log-sum-exp merge is the same fixed slice-order merge.
+ * Workspaces: >= 1024 B each (progress counters / status).  Errors as tim_logprob; tp must divide S_v.
+ * -------------------------------------------------------------------------- */
+tim_status tim_tp_vocab_range(int32_t vocab, int32_t tp, int32_t rank, int32_t* begin, int32_t* end);
+size_t tim_logprob_tp_partial_bytes(int64_t n_tok, int32_t vocab, int32_t tp);
+tim_status tim_logprob_tp_partial(const void* hidden_bf16, int64_t ld_hidden, const void* weight_shard_bf16,
+                                  int32_t hidden, int32_t vocab, int32_t tp, int32_t rank,
+                                  const int64_t* token_ids, int64_t n_tok,
+                                  float temperature, const float* temperatures_or_null,
+                                  void* partial_out, void* workspace, size_t workspace_bytes, void* stream);
+tim_status tim_logprob_tp_merge(const void* gathered_partials, int64_t n_tok, int32_t vocab,
+                                const int64_t* token_ids, const float* temperatures_or_null,
+                                float* logp_out, float* entropy_out_or_null,
+                                void* workspace, size_t workspace_bytes,
+                                tim_device_status* dstatus, void* stream);
+
+/* ----------------------------------------------------------------------------
  * tim_rmsnorm / tim_logprob_rmsnorm  (the batch-invariant RMSNorm
  * prologue of the head, §3.1)
  *

@@ -125,8 +125,10 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
                         const int64_t* ids, int64_t n_tok, float temperature, const float* temps, float* logp,
                         float* ent, void* ws, size_t ws_bytes, tim_device_status* dstatus, void* stream,
                         float* debug_logits, int64_t debug_ld, const uint64_t* row_keys = nullptr,
-                        uint64_t seed = 0, int64_t* ids_out = nullptr) {
+                        uint64_t seed = 0, int64_t* ids_out = nullptr, int32_t tp = 1, int32_t tp_rank = 0,
+                        void* tp_partial_out = nullptr) {
   const bool sample = row_keys != nullptr;
+  const bool tp_mode = tp_partial_out != nullptr;  // vocab-parallel rank: partials only, no merge
   if (!weight) return TIM_ERR_NULL;
   if (n_tok < 0 || n_tok >= (int64_t(1) << 31)) return TIM_ERR_SHAPE;
   if (d < 64 || d > 16384 || d % 64 != 0) return TIM_ERR_SHAPE;
@@ -135,12 +137,22 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   if (!(temperature > 0.f) || !std::isfinite(temperature)) return TIM_ERR_VALUE;
   if (!aligned(weight, 16) || (ld_hidden * 2) % 16 != 0) return TIM_ERR_ALIGN;
   if (n_tok == 0) return TIM_OK;  // empty batch: pointers may be NULL, nothing is launched
-  if (!hidden || !logp || (sample ? !ids_out : !ids)) return TIM_ERR_NULL;
+  if (!hidden || (!tp_mode && !logp) || (sample ? !ids_out : !ids)) return TIM_ERR_NULL;
   if (!aligned(hidden, 16)) return TIM_ERR_ALIGN;
   if (!ws) return TIM_ERR_NULL;
   if (!aligned(ws, 16)) return TIM_ERR_ALIGN;
-  if (ws_bytes < (sample ? tim_sample_workspace_bytes(n_tok, d, vocab) : tim_logprob_workspace_bytes(n_tok, d, vocab)))
-    return TIM_ERR_WORKSPACE;
+  const size_t ws_need = tp_mode ? kWsHeaderBytes
+                                 : (sample ? tim_sample_workspace_bytes(n_tok, d, vocab)
+                                           : tim_logprob_workspace_bytes(n_tok, d, vocab));
+  if (ws_bytes < ws_need) return TIM_ERR_WORKSPACE;
+  // fixed split of the full vocabulary; a tensor-parallel rank owns slices [s0, s1) = W rows [row0, row1)
+  const int32_t S_total = vocab_slices(vocab);
+  if (tp < 1 || S_total % tp != 0 || tp_rank < 0 || tp_rank >= tp) return TIM_ERR_SHAPE;
+  if (tp_mode && !aligned(tp_partial_out, 16)) return TIM_ERR_ALIGN;
+  const int32_t s0 = tp_rank * (S_total / tp), s1 = s0 + S_total / tp;
+  const int32_t nvt = n_vocab_tiles(vocab);
+  const int32_t row0 = tp_mode ? ((s0 * nvt) / S_total) * 256 : 0;
+  const int32_t row1 = tp_mode ? std::min(((s1 * nvt) / S_total) * 256, vocab) : vocab;
   DevInfo* dev = nullptr;
   tim_status st = device_info(&dev);
   if (st != TIM_OK) return st;
@@ -152,13 +164,13 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
                     dev->max_pair_clusters * 256.0 * d * 2.0 <= 0.75 * dev->l2_bytes;
   CUtensorMap th, tw;
   if (!encode_bf16_2d(&th, hidden, n_tok, d, ld_hidden, 128)) return TIM_ERR_CUDA;
-  if (!encode_bf16_2d(&tw, weight, vocab, d, d, quad ? fwd_w_box_rows(pair) / 2 : fwd_w_box_rows(pair)))
+  if (!encode_bf16_2d(&tw, weight, row1 - row0, d, d, quad ? fwd_w_box_rows(pair) / 2 : fwd_w_box_rows(pair)))
     return TIM_ERR_CUDA;
 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   uint8_t* wsb = static_cast<uint8_t*>(ws);
   WsHeader* hdr = reinterpret_cast<WsHeader*>(wsb);
-  float4* partials = reinterpret_cast<float4*>(wsb + kWsHeaderBytes);
+  float4* partials = tp_mode ? static_cast<float4*>(tp_partial_out) : reinterpret_cast<float4*>(wsb + kWsHeaderBytes);
   if (cudaMemsetAsync(hdr, 0, kWsHeaderBytes, s) != cudaSuccess) return TIM_ERR_CUDA;
 
   LogprobParams p{};
@@ -171,8 +183,11 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   p.hidden = d;
   const int unit = fwd_unit_rows(pair);
   p.n_mt = static_cast<int>((n_tok + unit - 1) / unit);
-  p.n_vt = n_vocab_tiles(vocab);
-  p.n_slices = vocab_slices(vocab);
+  p.n_vt = nvt;
+  p.n_slices = s1 - s0;
+  p.n_slices_total = S_total;
+  p.slice0 = s0;
+  p.w_row0 = row0;
   p.debug_logits = debug_logits;
   p.debug_ld = debug_ld;
   p.h_policy = g_h_policy;
@@ -207,6 +222,7 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   }
   if (launch_logprob_fwd(pair, debug_logits != nullptr, sample, quad, th, tw, p, grid, s) != cudaSuccess)
     return TIM_ERR_CUDA;
+  if (tp_mode) return TIM_OK;  // the caller all-gathers the slice partials, then tim_logprob_tp_merge
 
   MergeParams mp{};
   mp.partials = partials;
@@ -557,6 +573,62 @@ tim_status tim_comm_destroy(tim_comm* comm) {
   if (api->ok && comm->comm) api->destroy(comm->comm);
   delete comm;
   return TIM_OK;
+}
+
+// ------------------------------------------------ vocab-parallel (TP) head (NEXT-4) --
+tim_status tim_tp_vocab_range(int32_t vocab, int32_t tp, int32_t rank, int32_t* begin, int32_t* end) {
+  if (!begin || !end) return TIM_ERR_NULL;
+  if (vocab < 1 || tp < 1 || rank < 0 || rank >= tp) return TIM_ERR_SHAPE;
+  const int32_t S = vocab_slices(vocab);
+  if (S % tp != 0) return TIM_ERR_SHAPE;
+  const int32_t nvt = n_vocab_tiles(vocab);
+  const int32_t s0 = rank * (S / tp), s1 = s0 + S / tp;
+  *begin = ((s0 * nvt) / S) * 256;
+  *end = std::min(((s1 * nvt) / S) * 256, vocab);
+  return TIM_OK;
+}
+
+size_t tim_logprob_tp_partial_bytes(int64_t n_tok, int32_t vocab, int32_t tp) {
+  if (n_tok < 0 || vocab < 1 || tp < 1 || vocab_slices(vocab) % tp != 0) return 0;
+  return static_cast<size_t>(vocab_slices(vocab) / tp) * static_cast<size_t>(n_tok) * 16u;
+}
+
+tim_status tim_logprob_tp_partial(const void* hidden_bf16, int64_t ld_hidden, const void* weight_shard_bf16,
+                                  int32_t hidden, int32_t vocab, int32_t tp, int32_t rank, const int64_t* token_ids,
+                                  int64_t n_tok, float temperature, const float* temperatures_or_null,
+                                  void* partial_out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (n_tok > 0 && !partial_out) return TIM_ERR_NULL;
+  return logprob_impl(hidden_bf16, ld_hidden, weight_shard_bf16, hidden, vocab, token_ids, n_tok, temperature,
+                      temperatures_or_null, nullptr, nullptr, workspace, workspace_bytes, nullptr, stream, nullptr, 0,
+                      nullptr, 0, nullptr, tp, rank, partial_out);
+}
+
+tim_status tim_logprob_tp_merge(const void* gathered_partials, int64_t n_tok, int32_t vocab, const int64_t* token_ids,
+                                const float* temperatures_or_null, float* logp_out, float* entropy_out_or_null,
+                                void* workspace, size_t workspace_bytes, tim_device_status* dstatus, void* stream) {
+  if (n_tok < 0 || vocab < 1) return TIM_ERR_SHAPE;
+  if (n_tok == 0) return TIM_OK;
+  if (!gathered_partials || !token_ids || !logp_out || !workspace) return TIM_ERR_NULL;
+  if (!aligned(gathered_partials, 16) || !aligned(workspace, 16)) return TIM_ERR_ALIGN;
+  if (workspace_bytes < kWsHeaderBytes) return TIM_ERR_WORKSPACE;
+  DevInfo* dev = nullptr;
+  tim_status st = device_info(&dev);
+  if (st != TIM_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  WsHeader* hdr = static_cast<WsHeader*>(workspace);
+  if (cudaMemsetAsync(hdr, 0, kWsHeaderBytes, s) != cudaSuccess) return TIM_ERR_CUDA;
+  MergeParams mp{};
+  mp.partials = static_cast<const float4*>(gathered_partials);
+  mp.ids = token_ids;
+  mp.temps = temperatures_or_null;
+  mp.logp = logp_out;
+  mp.entropy = entropy_out_or_null;
+  mp.n_tok = n_tok;
+  mp.vocab = vocab;
+  mp.n_slices = vocab_slices(vocab);
+  mp.ws = hdr;
+  mp.dstatus = dstatus;
+  return launch_logprob_merge(mp, s) == cudaSuccess ? TIM_OK : TIM_ERR_CUDA;
 }
 
 // --------------------------------------------------------------- RMSNorm (NEXT-4) --

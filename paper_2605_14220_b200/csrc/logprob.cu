@@ -96,6 +96,13 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float c, int 
   u += (u4[0] + u4[1]) + (u4[2] + u4[3]);
 }
 
+// First vocab tile of local slice j: global slice slice0 + j of the fixed split of n_vt tiles into
+// n_slices_total slices (a function of V only -- the numerics contract).  A tensor-parallel rank
+// runs a contiguous subset of the slices against its shard of W (rows from w_row0 on).
+__device__ __forceinline__ int slice_tile(const LogprobParams& p, int j) {
+  return ((p.slice0 + j) * p.n_vt) / p.n_slices_total;
+}
+
 __device__ __forceinline__ uint64_t make_policy(int kind) {
   return kind == 3 ? policy_evict_last() : kind == 2 ? policy_evict_first() : policy_evict_normal();
 }
@@ -280,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int k = 0; sched.unit(cid, k, dm, j); ++k) {
       const int mt = dm * kNP + pid;
       const int m0 = mt * C::kUnitM + prank * kCtaM;
-      const int t0 = (j * p.n_vt) / n_slices, t1 = ((j + 1) * p.n_vt) / n_slices;
+      const int t0 = slice_tile(p, j), t1 = slice_tile(p, j + 1);
       for (int vt = t0; vt < t1; ++vt, ++step) {
         // bound the drift between pairs sweeping the same W tiles (performance only:
         // the wait is time-limited, results never depend on it)
@@ -291,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // timed-out wait
           if (known_min + p.sync_slack < step) gate = false;
         }
-        const int n0 = vt * kTileN + prank * C::kBRows + (kNP == 2 ? pid * (C::kBRows / 2) : 0);
+        const int n0 = vt * kTileN - p.w_row0 + prank * C::kBRows + (kNP == 2 ? pid * (C::kBRows / 2) : 0);
         for (int kb = 0; kb < nkb; ++kb) {
           if (p.sleep_waits) mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
           else mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
@@ -352,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t stage = 0, phase = 0, acc = 0, aphase = 0;
       int dm, j;
       for (int k = 0; sched.unit(cid, k, dm, j); ++k) {
-        const int t0 = (j * p.n_vt) / n_slices, t1 = ((j + 1) * p.n_vt) / n_slices;
+        const int t0 = slice_tile(p, j), t1 = slice_tile(p, j + 1);
         for (int vt = t0; vt < t1; ++vt) {
           mbar_wait(smem_u32(&tempty[acc]), aphase ^ 1);
           tc_fence_after();
@@ -399,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         rk_lo = static_cast<uint32_t>(rk);
         rk_hi = static_cast<uint32_t>(rk >> 32);
       }
-      const int t0 = (j * p.n_vt) / n_slices, t1 = ((j + 1) * p.n_vt) / n_slices;
+      const int t0 = slice_tile(p, j), t1 = slice_tile(p, j + 1);
       for (int vt = t0; vt < t1; ++vt) {
         if (p.sleep_waits) mbar_wait_sleep(smem_u32(&tfull[acc]), aphase);
         else mbar_wait(smem_u32(&tfull[acc]), aphase);

@@ -32,7 +32,10 @@ struct LogprobParams {
   int hidden;
   int n_mt;
   int n_vt;
-  int n_slices;
+  int n_slices;         // slices this launch runs (all of them unless tensor-parallel)
+  int n_slices_total;   // S_v of the full vocabulary
+  int slice0;           // first global slice of this launch
+  int w_row0;           // first W row present in the weight tensor (tensor-parallel shard)
   float* debug_logits;  // test-only raw fp32 accumulators [n_tok][debug_ld]
   int64_t debug_ld;
   int h_policy;         // L2 eviction policy of H / W tile loads: 0 none, 1 normal, 2 first, 3 last

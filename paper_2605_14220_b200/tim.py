@@ -78,6 +78,10 @@ _SIGS = {
     "tim_correct_partial_bytes": (_SZ, [_I64]),
     "tim_correct_local": (_I32, [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "tim_correct_finish": (_I32, [_P, _I32, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P]),
+    "tim_tp_vocab_range": (_I32, [_I32, _I32, _I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
+    "tim_logprob_tp_partial_bytes": (_SZ, [_I64, _I32, _I32]),
+    "tim_logprob_tp_partial": (_I32, [_P, _I64, _P, _I32, _I32, _I32, _I32, _P, _I64, _F, _P, _P, _P, _SZ, _P]),
+    "tim_logprob_tp_merge": (_I32, [_P, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _P, _P]),
     "tim_rmsnorm": (_I32, [_P, _I64, _P, _F, _I32, _I64, _P, _P]),
     "tim_logprob_rmsnorm_workspace_bytes": (_SZ, [_I64, _I32, _I32]),
     "tim_logprob_rmsnorm": (_I32, [_P, _I64, _P, _F, _P, _I32, _I32, _P, _I64, _F, _P, _P, _P, _P, _SZ, _P, _P]),
@@ -277,6 +281,44 @@ def sample(hidden: torch.Tensor, weight: torch.Tensor, row_keys: torch.Tensor, s
                         ctypes.c_uint64(int(seed) % (1 << 64)), float(temperature), _ptr(temperatures), _ptr(ids),
                         _ptr(lp), _ptr(ent), _ptr(ws), ws.numel(), _ptr(status), _stream(dev)), "tim_sample")
     return ids, lp, ent
+
+
+def tp_vocab_range(vocab: int, tp: int, rank: int) -> tuple[int, int]:
+    """W rows [begin, end) owned by `rank` of a `tp`-way vocab-parallel head (whole slices)."""
+    b, e = _I32(), _I32()
+    _check(lib().tim_tp_vocab_range(vocab, tp, rank, ctypes.byref(b), ctypes.byref(e)), "tim_tp_vocab_range")
+    return b.value, e.value
+
+
+def logprob_tp_partial(hidden: torch.Tensor, weight_shard: torch.Tensor, vocab: int, tp: int, rank: int,
+                       ids: torch.Tensor, temperature: float = 1.0, temperatures: torch.Tensor | None = None):
+    """One rank of a vocab-parallel head: this rank's slice partials (uint8 block) -- tim_logprob_tp_partial."""
+    dev = hidden.device
+    N, d = hidden.shape
+    weight_shard = weight_shard.contiguous()
+    ids = ids.to(device=dev, dtype=torch.int64).contiguous()
+    if temperatures is not None:
+        temperatures = temperatures.to(device=dev, dtype=torch.float32).contiguous()
+    L = lib()
+    part = torch.empty(max(1, int(L.tim_logprob_tp_partial_bytes(N, vocab, tp))), dtype=torch.uint8, device=dev)
+    ws = _workspace(dev, 1024, "tp")
+    _check(L.tim_logprob_tp_partial(_ptr(hidden), hidden.stride(0), _ptr(weight_shard), d, vocab, tp, rank, _ptr(ids),
+                                    N, float(temperature), _ptr(temperatures), _ptr(part), _ptr(ws), ws.numel(),
+                                    _stream(dev)), "tim_logprob_tp_partial")
+    return part
+
+
+def logprob_tp_merge(gathered: torch.Tensor, n_tok: int, vocab: int, ids: torch.Tensor,
+                     temperatures: torch.Tensor | None = None, status: torch.Tensor | None = None):
+    """Merge the all-gathered slice partials of every rank -- tim_logprob_tp_merge."""
+    dev = gathered.device
+    ids = ids.to(device=dev, dtype=torch.int64).contiguous()
+    lp = torch.empty(n_tok, dtype=torch.float32, device=dev)
+    ent = torch.empty(n_tok, dtype=torch.float32, device=dev)
+    ws = _workspace(dev, 1024, "tp_merge")
+    _check(lib().tim_logprob_tp_merge(_ptr(gathered), n_tok, vocab, _ptr(ids), _ptr(temperatures), _ptr(lp), _ptr(ent),
+                                      _ptr(ws), ws.numel(), _ptr(status), _stream(dev)), "tim_logprob_tp_merge")
+    return lp, ent
 
 
 def rmsnorm(hidden: torch.Tensor, gamma: torch.Tensor, eps: float = 1e-6) -> torch.Tensor:

@@ -126,3 +126,15 @@ def test_shard_range_covers_tokens():
             assert cuts[0][0] == 0 and cuts[-1][1] == n
             for (a, b), (c, d) in zip(cuts[:-1], cuts[1:]):
                 assert b == c and a <= b
+
+
+def test_tp_vocab_ranges_partition_the_vocabulary():
+    for V in (300, 1000, 4096, 151936, 152064):
+        S = tim.lib().tim_logprob_vocab_slices(V)
+        for tp in (1, 2, 4, 8):
+            if S % tp:
+                continue
+            rs = [tim.tp_vocab_range(V, tp, r) for r in range(tp)]
+            assert rs[0][0] == 0 and rs[-1][1] == V
+            for (a, b), (c, d) in zip(rs[:-1], rs[1:]):
+                assert b == c and a % 256 == 0 and a < b
