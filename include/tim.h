@@ -310,6 +310,35 @@ tim_status tim_logprob_rmsnorm(const void* hidden_bf16, int64_t ld_hidden, const
                                tim_device_status* dstatus, void* stream);
 
 /* ----------------------------------------------------------------------------
+ * tim_head_backward  (backward of the head; the "score function
+ * gradient" the trainer takes through logp, §3)
+ *
+ * For the scalar L = sum_t g_t logp_t + e_t H_t (g = grad_logp, e = grad_ent_or_null or 0) with
+ * z = h W^T, y = z / T_t, p = softmax(y), logp_t = y[a_t] - lse(y), H_t = -sum_v p ln p:
+ *   G[t, v]     = dL/dz[t, v] = (1/T_t) [ g_t (1[v = a_t] - p_v) - e_t p_v (ln p_v + H_t) ]
+ *   dhidden[t]  = sum_v G[t, v] W[v]         (fp32 [n_tok, hidden], contiguous; overwritten)
+ *   dweight[v]  = sum_t G[t, v] h[t]         (fp32 [vocab, hidden], contiguous; overwritten)
+ * Path: tim_logprob's kernel (forward: logp, H, log2-sum-exp per token), the same tcgen05 kernel
+ * again with a gradient epilogue that writes G as bf16 into the workspace (logits never reach
+ * HBM), then two cuBLAS bf16 GEMMs with fp32 accumulation (libcublas loaded at run time;
+ * TIM_ERR_UNSUPPORTED if it cannot be loaded).  Tokens are processed in blocks whose bf16 G
+ * block fits 4 GiB; dweight accumulates over the blocks in block order (fp32).
+ * Deterministic run to run on one device; NOT batch-invariant (cuBLAS picks its kernel by
+ * shape, and G is rounded to bf16 before the GEMMs).
+ * Inputs and errors as tim_logprob (bad id / temperature -> TIM_ERR_DATA with the global token
+ * index); either output may be NULL (skipped), not both.  n_tok == 0 zeroes dweight.
+ * workspace >= tim_head_backward_workspace_bytes(n_tok, hidden, vocab), 256-B aligned.
+ * -------------------------------------------------------------------------- */
+size_t tim_head_backward_workspace_bytes(int64_t n_tok, int32_t hidden, int32_t vocab);
+tim_status tim_head_backward(const void* hidden_bf16, int64_t ld_hidden, const void* weight_bf16,
+                             int32_t hidden, int32_t vocab, const int64_t* token_ids, int64_t n_tok,
+                             float temperature, const float* temperatures_or_null,
+                             const float* grad_logp, const float* grad_ent_or_null,
+                             float* dhidden_or_null, float* dweight_or_null,
+                             void* workspace, size_t workspace_bytes,
+                             tim_device_status* dstatus, void* stream);
+
+/* ----------------------------------------------------------------------------
  * tim_ppo_loss  (fused PPO / GRPO surrogate + loss diagnostics)
  *
  * Per token t (PAPER.md eq:ppo_loss P:352-360, eq:ppo_ratio P:361-373, App. A.4):

@@ -7,6 +7,6 @@ the package fails loudly if the library is missing.
 """
 from .tim import (  # noqa: F401
     CorrectConfig, Comm, TimError, PRESETS, PPOConfig, logprob, sample, correct, mismatch_stats, correct_local,
-    ppo_loss, ppo_local, ppo_finish, rmsnorm, logprob_rmsnorm, tp_vocab_range, logprob_tp_partial, logprob_tp_merge,
+    ppo_loss, ppo_local, ppo_finish, rmsnorm, logprob_rmsnorm, head_backward, tp_vocab_range, logprob_tp_partial, logprob_tp_merge,
     correct_finish, exchange_partials, lib, library_path, shard_range, vocab_slices,
 )

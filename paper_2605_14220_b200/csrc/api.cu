@@ -121,12 +121,25 @@ inline int32_t vocab_slices(int32_t vocab) {
   return nvt < kMaxSlices ? nvt : kMaxSlices;
 }
 
+int pick_group(const DevInfo* dev, bool pair, int n_slices, int64_t groups, int32_t d) {
+  int g = 1;
+  if (pair && g_group > 0) {
+    if (n_slices % g_group == 0 && groups >= g_group) g = g_group;
+  } else if (pair) {
+    const double h_tile = 256.0 * d * 2.0;
+    while (g < 8 && n_slices % (g * 2) == 0 && groups >= g * 2 &&
+           (static_cast<double>(groups) / g) * h_tile > 0.75 * dev->l2_bytes)
+      g *= 2;
+  }
+  return g;
+}
+
 tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weight, int32_t d, int32_t vocab,
                         const int64_t* ids, int64_t n_tok, float temperature, const float* temps, float* logp,
                         float* ent, void* ws, size_t ws_bytes, tim_device_status* dstatus, void* stream,
                         float* debug_logits, int64_t debug_ld, const uint64_t* row_keys = nullptr,
                         uint64_t seed = 0, int64_t* ids_out = nullptr, int32_t tp = 1, int32_t tp_rank = 0,
-                        void* tp_partial_out = nullptr) {
+                        void* tp_partial_out = nullptr, float* lse2_out = nullptr, int64_t index_base = 0) {
   const bool sample = row_keys != nullptr;
   const bool tp_mode = tp_partial_out != nullptr;  // vocab-parallel rank: partials only, no merge
   if (!weight) return TIM_ERR_NULL;
@@ -209,17 +222,7 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   // Pairs sharing an M-tile: smallest G in {1, 2, 4, 8} (dividing S_v, <= #pairs) whose live H
   // tiles (one 256-row tile per group) fit in ~75% of L2.  Performance only: which pair runs
   // which (M-tile, slice) unit never changes a row's arithmetic.
-  p.group = 1;
-  if (quad) {
-    p.group = 1;
-  } else if (pair && g_group > 0) {
-    if (p.n_slices % g_group == 0 && groups >= g_group) p.group = g_group;
-  } else if (pair) {
-    const double h_tile = 256.0 * d * 2.0;
-    while (p.group < 8 && p.n_slices % (p.group * 2) == 0 && groups >= p.group * 2 &&
-           (static_cast<double>(groups) / p.group) * h_tile > 0.75 * dev->l2_bytes)
-      p.group *= 2;
-  }
+  p.group = quad ? 1 : pick_group(dev, pair, p.n_slices, groups, d);
   if (launch_logprob_fwd(pair, debug_logits != nullptr, sample, quad, th, tw, p, grid, s) != cudaSuccess)
     return TIM_ERR_CUDA;
   if (tp_mode) return TIM_OK;  // the caller all-gathers the slice partials, then tim_logprob_tp_merge
@@ -237,6 +240,8 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   mp.dstatus = dstatus;
   mp.partials2 = p.partials2;
   mp.ids_out = ids_out;
+  mp.lse2_out = lse2_out;
+  mp.index_base = index_base;
   if ((sample ? launch_sample_merge(mp, s) : launch_logprob_merge(mp, s)) != cudaSuccess) return TIM_ERR_CUDA;
   return TIM_OK;
 }
@@ -311,6 +316,57 @@ NcclApi* nccl() {
   return &api;
 }
 constexpr int kNcclInt8 = 0;
+
+// ------------------------------------------------------------------ cuBLAS --
+// The two plain GEMMs of the head backward (dH = G W, dW = G^T H) go to cuBLAS, loaded at run
+// time (libcublas.so.12, the one torch already mapped when present).  Deterministic run to run.
+typedef void* cublas_handle_t;
+typedef int (*PFN_cublasCreate)(cublas_handle_t*);
+typedef int (*PFN_cublasSetStream)(cublas_handle_t, cudaStream_t);
+typedef int (*PFN_cublasGemmEx)(cublas_handle_t, int, int, int, int, int, const void*, const void*, int, int,
+                                const void*, int, int, const void*, void*, int, int, int, int);
+struct CublasApi {
+  bool ok = false;
+  PFN_cublasCreate create = nullptr;
+  PFN_cublasSetStream set_stream = nullptr;
+  PFN_cublasGemmEx gemm_ex = nullptr;
+  cublas_handle_t handle[kMaxDev] = {};
+};
+CublasApi* cublas() {
+  static CublasApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libcublas.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.create = reinterpret_cast<PFN_cublasCreate>(dlsym(h, "cublasCreate_v2"));
+    api.set_stream = reinterpret_cast<PFN_cublasSetStream>(dlsym(h, "cublasSetStream_v2"));
+    api.gemm_ex = reinterpret_cast<PFN_cublasGemmEx>(dlsym(h, "cublasGemmEx"));
+    api.ok = api.create && api.set_stream && api.gemm_ex;
+  });
+  return &api;
+}
+constexpr int kCublasOpN = 0, kCublasOpT = 1, kCudaR32F = 0, kCudaR16BF = 14, kCublasCompute32F = 68,
+              kCublasGemmDefault = -1;
+
+// column-major C[m x n] = alpha op(A) op(B) + beta C, bf16 inputs, fp32 accumulate / output
+tim_status gemm_bf16_f32(cudaStream_t s, int opa, int opb, int m, int n, int k, const void* A, int lda, const void* B,
+                         int ldb, float beta, float* C, int ldc) {
+  CublasApi* api = cublas();
+  if (!api->ok) return TIM_ERR_UNSUPPORTED;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= kMaxDev) return TIM_ERR_CUDA;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!api->handle[dev] && api->create(&api->handle[dev]) != 0) return TIM_ERR_CUDA;
+  }
+  if (api->set_stream(api->handle[dev], s) != 0) return TIM_ERR_CUDA;
+  const float alpha = 1.0f;
+  return api->gemm_ex(api->handle[dev], opa, opb, m, n, k, &alpha, A, kCudaR16BF, lda, B, kCudaR16BF, ldb, &beta, C,
+                      kCudaR32F, ldc, kCublasCompute32F, kCublasGemmDefault) == 0
+             ? TIM_OK
+             : TIM_ERR_CUDA;
+}
 
 }  // namespace
 
@@ -672,6 +728,132 @@ tim_status tim_logprob_rmsnorm(const void* hidden, int64_t ld_hidden, const void
   if (st != TIM_OK) return st;
   return tim_logprob(n_tok ? x : nullptr, d, weight, d, vocab, ids, n_tok, temperature, temps, logp, ent,
                      n_tok ? static_cast<uint8_t*>(ws) + xb : nullptr, n_tok ? ws_bytes - xb : 0, dstatus, stream);
+}
+
+// ------------------------------------------------------------------ head backward (NEXT-3) --
+static int64_t bwd_g_ld(int32_t vocab) { return (static_cast<int64_t>(vocab) + 7) & ~int64_t(7); }
+static int64_t bwd_block_rows(int64_t n_tok, int32_t vocab) {
+  constexpr double kGBudget = 4294967296.0;  // bf16 G block <= 4 GiB
+  int64_t nb = static_cast<int64_t>(kGBudget / (2.0 * static_cast<double>(bwd_g_ld(vocab))));
+  nb = nb / 256 * 256;
+  if (nb < 256) nb = 256;
+  const int64_t need = (n_tok + 255) / 256 * 256;
+  return need < nb ? need : nb;
+}
+static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+size_t tim_head_backward_workspace_bytes(int64_t n_tok, int32_t hidden, int32_t vocab) {
+  if (n_tok < 0 || vocab < 1) return 0;
+  if (n_tok == 0) return 0;
+  const int64_t nb = bwd_block_rows(n_tok, vocab);
+  return al256(tim_logprob_workspace_bytes(nb, hidden, vocab)) + 3 * al256(static_cast<size_t>(nb) * 4u) +
+         static_cast<size_t>(nb) * static_cast<size_t>(bwd_g_ld(vocab)) * 2u;
+}
+
+tim_status tim_head_backward(const void* hidden_bf16, int64_t ld_hidden, const void* weight_bf16, int32_t d,
+                             int32_t vocab, const int64_t* token_ids, int64_t n_tok, float temperature,
+                             const float* temps, const float* grad_logp, const float* grad_ent_or_null,
+                             float* dhidden_or_null, float* dweight_or_null, void* ws, size_t ws_bytes,
+                             tim_device_status* dstatus, void* stream) {
+  if (!weight_bf16) return TIM_ERR_NULL;
+  if (n_tok < 0 || n_tok >= (int64_t(1) << 31)) return TIM_ERR_SHAPE;
+  if (d < 64 || d > 16384 || d % 64 != 0) return TIM_ERR_SHAPE;
+  if (vocab < 1 || vocab > (1 << 24)) return TIM_ERR_SHAPE;
+  if (ld_hidden < d) return TIM_ERR_SHAPE;
+  if (!(temperature > 0.f) || !std::isfinite(temperature)) return TIM_ERR_VALUE;
+  if (!aligned(weight_bf16, 16) || (ld_hidden * 2) % 16 != 0) return TIM_ERR_ALIGN;
+  if (!dhidden_or_null && !dweight_or_null) return TIM_ERR_NULL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (dweight_or_null && !aligned(dweight_or_null, 16)) return TIM_ERR_ALIGN;
+  if (n_tok == 0) {  // dL/dW of an empty batch is 0; nothing else to do
+    if (dweight_or_null &&
+        cudaMemsetAsync(dweight_or_null, 0, static_cast<size_t>(vocab) * d * 4u, s) != cudaSuccess)
+      return TIM_ERR_CUDA;
+    return TIM_OK;
+  }
+  if (!hidden_bf16 || !token_ids || !grad_logp || !ws) return TIM_ERR_NULL;
+  if (!aligned(hidden_bf16, 16) || !aligned(ws, 256)) return TIM_ERR_ALIGN;
+  if (dhidden_or_null && !aligned(dhidden_or_null, 16)) return TIM_ERR_ALIGN;
+  if (ws_bytes < tim_head_backward_workspace_bytes(n_tok, d, vocab)) return TIM_ERR_WORKSPACE;
+  DevInfo* dev = nullptr;
+  tim_status st = device_info(&dev);
+  if (st != TIM_OK) return st;
+  if (!cublas()->ok) return TIM_ERR_UNSUPPORTED;
+
+  const int64_t nb = bwd_block_rows(n_tok, vocab), g_ld = bwd_g_ld(vocab);
+  uint8_t* w8 = static_cast<uint8_t*>(ws);
+  const size_t fwd_bytes = al256(tim_logprob_workspace_bytes(nb, d, vocab));
+  uint8_t* fwd_ws = w8;
+  float* logp = reinterpret_cast<float*>(w8 + fwd_bytes);
+  float* ent = reinterpret_cast<float*>(w8 + fwd_bytes + al256(nb * 4));
+  float* lse2 = reinterpret_cast<float*>(w8 + fwd_bytes + 2 * al256(nb * 4));
+  uint16_t* G = reinterpret_cast<uint16_t*>(w8 + fwd_bytes + 3 * al256(nb * 4));
+  const int32_t S = vocab_slices(vocab);
+  const int32_t nvt = n_vocab_tiles(vocab);
+  CUtensorMap tw;
+  if (!encode_bf16_2d(&tw, weight_bf16, vocab, d, d, fwd_w_box_rows(true))) return TIM_ERR_CUDA;
+  if (dweight_or_null &&
+      cudaMemsetAsync(dweight_or_null, 0, static_cast<size_t>(vocab) * d * 4u, s) != cudaSuccess)
+    return TIM_ERR_CUDA;
+
+  for (int64_t b0 = 0; b0 < n_tok; b0 += nb) {
+    const int64_t nbc = (n_tok - b0 < nb) ? n_tok - b0 : nb;
+    const void* hb = static_cast<const uint8_t*>(hidden_bf16) + b0 * ld_hidden * 2;
+    const float* tb = temps ? temps + b0 : nullptr;
+    // (1) forward: logp, H, log2-sum-exp of the block (the same kernel and numerics as tim_logprob)
+    st = logprob_impl(hb, ld_hidden, weight_bf16, d, vocab, token_ids + b0, nbc, temperature, tb, logp, ent,
+                      fwd_ws, fwd_bytes, dstatus, stream, nullptr, 0, nullptr, 0, nullptr, 1, 0, nullptr, lse2, b0);
+    if (st != TIM_OK) return st;
+    // (2) recompute the logits tile by tile; the epilogue writes G = dL/dz (bf16) instead of LSE partials
+    CUtensorMap th;
+    if (!encode_bf16_2d(&th, hb, nbc, d, ld_hidden, 128)) return TIM_ERR_CUDA;
+    if (cudaMemsetAsync(fwd_ws, 0, kWsHeaderBytes, s) != cudaSuccess) return TIM_ERR_CUDA;
+    LogprobParams p{};
+    p.ids = token_ids + b0;
+    p.temps = tb;
+    p.temperature = temperature;
+    p.partials = reinterpret_cast<float4*>(fwd_ws + kWsHeaderBytes);  // not written in gradient mode
+    p.n_tok = static_cast<int>(nbc);
+    p.vocab = vocab;
+    p.hidden = d;
+    p.n_mt = static_cast<int>((nbc + fwd_unit_rows(true) - 1) / fwd_unit_rows(true));
+    p.n_vt = nvt;
+    p.n_slices = S;
+    p.n_slices_total = S;
+    p.h_policy = g_h_policy;
+    p.w_policy = g_w_policy;
+    p.sleep_waits = g_sleep_waits;
+    p.progress = reinterpret_cast<uint32_t*>(fwd_ws + kWsProgressOffset);
+    p.sync_slack = g_sync_slack;
+    p.hidden_ptr = hb;
+    p.ld_hidden_bytes = ld_hidden * 2;
+    p.grad_logp = grad_logp + b0;
+    p.grad_ent = grad_ent_or_null ? grad_ent_or_null + b0 : nullptr;
+    p.ent_in = ent;
+    p.lse2_in = lse2;
+    p.g_out = G;
+    p.g_ld = g_ld;
+    p.g_col0 = 0;
+    const int64_t n_units = static_cast<int64_t>(p.n_mt) * S;
+    int64_t cap = dev->max_pair_clusters;
+    if (g_max_clusters > 0 && g_max_clusters < cap) cap = g_max_clusters;
+    const int64_t groups = n_units < cap ? n_units : cap;
+    p.group = pick_group(dev, true, S, groups, d);
+    if (launch_head_grad(th, tw, p, static_cast<int>(groups * 2), s) != cudaSuccess) return TIM_ERR_CUDA;
+    // (3) dH[b] = G W  (column-major: dH^T[d x nbc] = W^T[d x V] G^T[V x nbc])
+    if (dhidden_or_null) {
+      st = gemm_bf16_f32(s, kCublasOpN, kCublasOpN, d, static_cast<int>(nbc), vocab, weight_bf16, d, G,
+                         static_cast<int>(g_ld), 0.0f, dhidden_or_null + b0 * d, d);
+      if (st != TIM_OK) return st;
+    }
+    // (4) dW += G^T H[b]  (column-major: dW^T[d x V] += H^T[d x nbc] G[nbc x V])
+    if (dweight_or_null) {
+      st = gemm_bf16_f32(s, kCublasOpN, kCublasOpT, d, vocab, static_cast<int>(nbc), hb,
+                         static_cast<int>(ld_hidden), G, static_cast<int>(g_ld), 1.0f, dweight_or_null, d);
+      if (st != TIM_OK) return st;
+    }
+  }
+  return TIM_OK;
 }
 
 // ------------------------------------------------------------------ PPO (NEXT-2) --

@@ -15,6 +15,7 @@
 // of these enter the arithmetic of a row.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
 #include <math_constants.h>
 
 #include <cstdint>
@@ -223,7 +224,43 @@ __device__ __noinline__ uint32_t wait_progress(const uint32_t* prog, uint32_t nc
 
 // kNP = CTA pairs per cluster: 1 (cluster of 2) or 2 (cluster of 4: the two pairs own different
 // M-tiles, sweep the same vocab tiles in lock-step and share every W tile through TMA multicast).
-template <bool kPair, bool kDebug, bool kSample, int kNP>
+// ------------------------------------------------------------ head backward (NEXT-3) --
+// G[t, v] = dL/dz[t, v] = (1/T) [ g (1[v = a] - p) - e p (ln p + H) ] for L = sum_t g_t logp_t +
+// e_t H_t, with p = 2^(y - lse2) from the forward's log2-sum-exp; written as bf16 to the slice's
+// G block (row-major, ld = p.g_ld) for the two library GEMMs dH = G W and dW = G^T H.
+__device__ __forceinline__ void grad_chunk(const uint32_t (&r)[32], float c, int col0, int vocab, int64_t a,
+                                           float gl, float ge, float gH, float lse2, float invT,
+                                           const LogprobParams& p, int row) {
+  constexpr float kLn2 = 0.69314718055994530942f;
+  uint32_t packed[16];
+#pragma unroll
+  for (int i = 0; i < 32; i += 2) {
+    float gv[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const float t = fmaf(__uint_as_float(r[i + q]), c, -lse2);  // log2 p
+      const float pr = ex2_approx(t);
+      float g = pr * (-gl - ge * fmaf(t, kLn2, gH));
+      if (a == col0 + i + q) g += gl;
+      gv[q] = g * invT;
+    }
+    const __nv_bfloat162 b = __floats2bfloat162_rn(gv[0], gv[1]);
+    packed[i / 2] = *reinterpret_cast<const uint32_t*>(&b);
+  }
+  const int lc0 = col0 - p.g_col0;  // column inside this slice's G block
+  uint16_t* dst = p.g_out + static_cast<int64_t>(row) * p.g_ld + lc0;
+  if (col0 + 32 <= vocab) {
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+      d4[v] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+  } else {
+    for (int i = 0; i < 32 && col0 + i < vocab; ++i)
+      dst[i] = static_cast<uint16_t>(packed[i / 2] >> (16 * (i & 1)));
+  }
+}
+
+template <bool kPair, bool kDebug, bool kSample, int kNP, bool kGrad = false>
 __global__ void __launch_bounds__(kThreads, 1)
     logprob_fwd_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constant__ CUtensorMap tmap_w,
                        LogprobParams p) {
@@ -398,6 +435,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float T = (valid && p.temps) ? __ldg(p.temps + row) : p.temperature;
       const float c = __fdiv_rn(kLog2eF, T);
       float m = -CUDART_INF_F, s = 0.f, uu = 0.f, ya = -CUDART_INF_F;
+      float gl = 0.f, ge = 0.f, gH = 0.f, lse2 = 0.f, invT = 0.f;  // gradient mode (NEXT-3)
+      if (kGrad && valid) {
+        gl = __ldg(p.grad_logp + row);
+        ge = p.grad_ent ? __ldg(p.grad_ent + row) : 0.f;
+        gH = __ldg(p.ent_in + row);
+        lse2 = __ldg(p.lse2_in + row);
+        invT = __fdiv_rn(1.0f, T);
+      }
       float best_s = -CUDART_INF_F, best_y = -CUDART_INF_F;
       int best_col = -1;
       uint32_t rk_lo = 0, rk_hi = 0;
@@ -430,7 +475,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 32; ++i)
               if (col0 + i < p.vocab) dst[i] = __uint_as_float(r[i]);
           }
-          if (tail_tile)
+          if (kGrad) {
+            if (valid) grad_chunk(r, c, col0, p.vocab, a, gl, ge, gH, lse2, invT, p, row);
+          } else if (tail_tile)
             epi_chunk<true>(r, c, col0, p.vocab, a, m, s, uu, ya);
           else
             epi_chunk<false>(r, c, col0, p.vocab, a, m, s, uu, ya);
@@ -445,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc ^= 1;
         if (acc == 0) aphase ^= 1;
       }
-      if (valid) {
+      if (valid && !kGrad) {
         p.partials[static_cast<int64_t>(j) * p.n_tok + row] = make_float4(m, s, uu, ya);
         if (kSample)
           p.partials2[static_cast<int64_t>(j) * p.n_tok + row] =
@@ -486,10 +533,11 @@ __global__ void __launch_bounds__(256) logprob_merge_kernel(MergeParams p) {
     }
     const double l2s = log2(S);
     const double kLn2 = 0.69314718055994530942;
+    if (p.lse2_out) p.lse2_out[t] = static_cast<float>(M + l2s);
     p.logp[t] = bad ? CUDART_NAN_F : static_cast<float>(kLn2 * ((ya - M) - l2s));
     if (p.entropy) p.entropy[t] = static_cast<float>(kLn2 * (l2s - U / S));
     if (bad) atomicMax(reinterpret_cast<unsigned long long*>(&p.ws->bad_inv),
-                       static_cast<unsigned long long>(kBadSentinel - t));
+                       static_cast<unsigned long long>(kBadSentinel - (t + p.index_base)));
   }
   commit_status_last_block(p.ws, p.dstatus);
 }
@@ -534,11 +582,11 @@ __global__ void __launch_bounds__(256) sample_merge_kernel(MergeParams p) {
   commit_status_last_block(p.ws, p.dstatus);
 }
 
-template <bool kPair, bool kDebug, bool kSample, int kNP>
+template <bool kPair, bool kDebug, bool kSample, int kNP, bool kGrad = false>
 static cudaError_t launch_fwd(const CUtensorMap& th, const CUtensorMap& tw, const LogprobParams& p, int grid,
                               cudaStream_t stream) {
   using C = KCfg<kPair>;
-  auto kern = logprob_fwd_kernel<kPair, kDebug, kSample, kNP>;
+  auto kern = logprob_fwd_kernel<kPair, kDebug, kSample, kNP, kGrad>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
@@ -562,6 +610,11 @@ static cudaError_t launch_fwd(const CUtensorMap& th, const CUtensorMap& tw, cons
 
 int fwd_unit_rows(bool pair) { return pair ? KCfg<true>::kUnitM : KCfg<false>::kUnitM; }
 int fwd_w_box_rows(bool pair) { return pair ? KCfg<true>::kBRows : KCfg<false>::kBRows; }
+
+cudaError_t launch_head_grad(const CUtensorMap& th, const CUtensorMap& tw, const LogprobParams& p, int grid,
+                             cudaStream_t stream) {
+  return launch_fwd<true, false, false, 1, true>(th, tw, p, grid, stream);
+}
 
 cudaError_t launch_logprob_fwd(bool pair, bool debug, bool sample, bool quad, const CUtensorMap& th,
                                const CUtensorMap& tw, const LogprobParams& p, int grid, cudaStream_t stream) {

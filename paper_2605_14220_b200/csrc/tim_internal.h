@@ -50,6 +50,14 @@ struct LogprobParams {
   const void* hidden_ptr;    // H base (for L2 priority demotion of finished M-tiles)
   int64_t ld_hidden_bytes;
   int demote;                // demote finished H tiles to evict_normal
+  // head backward (NEXT-3) gradient epilogue
+  const float* grad_logp;    // [n_tok] dL/dlogp
+  const float* grad_ent;     // [n_tok] dL/dH or null
+  const float* ent_in;       // [n_tok] entropy (nats) from the forward
+  const float* lse2_in;      // [n_tok] log2-sum-exp of y = z log2(e) / T from the forward
+  uint16_t* g_out;           // bf16 G block of the current slice, [n_tok][g_ld]
+  int64_t g_ld;
+  int g_col0;                // first vocab column of the G block
 };
 
 struct MergeParams {
@@ -65,6 +73,8 @@ struct MergeParams {
   tim_device_status* dstatus;
   const float4* partials2;  // sampling twin
   int64_t* ids_out;         // sampling twin
+  float* lse2_out;          // head backward: per-token log2-sum-exp (may be null)
+  int64_t index_base;       // added to a bad token's index in the status (token-blocked callers)
 };
 
 // Commit the call's data-error state to the caller's status word; executed by the last block
@@ -100,6 +110,8 @@ int fwd_w_box_rows(bool pair);
 cudaError_t launch_logprob_fwd(bool pair, bool debug, bool sample, bool quad, const CUtensorMap& th,
                                const CUtensorMap& tw, const LogprobParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_logprob_merge(const MergeParams& p, cudaStream_t stream);
+cudaError_t launch_head_grad(const CUtensorMap& th, const CUtensorMap& tw, const LogprobParams& p, int grid,
+                             cudaStream_t stream);
 cudaError_t launch_sample_merge(const MergeParams& p, cudaStream_t stream);
 
 // correct.cu

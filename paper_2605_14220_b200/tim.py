@@ -85,6 +85,8 @@ _SIGS = {
     "tim_rmsnorm": (_I32, [_P, _I64, _P, _F, _I32, _I64, _P, _P]),
     "tim_logprob_rmsnorm_workspace_bytes": (_SZ, [_I64, _I32, _I32]),
     "tim_logprob_rmsnorm": (_I32, [_P, _I64, _P, _F, _P, _I32, _I32, _P, _I64, _F, _P, _P, _P, _P, _SZ, _P, _P]),
+    "tim_head_backward_workspace_bytes": (_SZ, [_I64, _I32, _I32]),
+    "tim_head_backward": (_I32, [_P, _I64, _P, _I32, _I32, _P, _I64, _F, _P, _P, _P, _P, _P, _P, _SZ, _P, _P]),
     "tim_ppo_partial_bytes": (_SZ, [_I64, _I32]),
     "tim_ppo_workspace_bytes": (_SZ, [_I64, _I32, _I32]),
     "tim_ppo_loss": (_I32, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P,
@@ -351,6 +353,39 @@ def logprob_rmsnorm(hidden: torch.Tensor, gamma: torch.Tensor, weight: torch.Ten
                                  _ptr(ids), N, float(temperature), _ptr(temperatures), _ptr(lp), _ptr(ent), _ptr(ws),
                                  ws.numel(), _ptr(status), _stream(dev)), "tim_logprob_rmsnorm")
     return lp, ent
+
+
+def head_backward(hidden: torch.Tensor, weight: torch.Tensor, ids: torch.Tensor, grad_logp: torch.Tensor,
+                  grad_entropy: torch.Tensor | None = None, temperature: float = 1.0,
+                  temperatures: torch.Tensor | None = None, need_dhidden: bool = True, need_dweight: bool = True,
+                  status: torch.Tensor | None = None):
+    """Backward of the head for L = sum_t grad_logp[t] logp_t + grad_entropy[t] H_t -- tim_head_backward.
+
+    Returns (dhidden fp32 [N, d] or None, dweight fp32 [V, d] or None)."""
+    dev = hidden.device
+    if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
+        raise TypeError("hidden and weight must be bfloat16")
+    if hidden.dim() != 2 or hidden.stride(1) != 1:
+        raise ValueError("hidden must be [N, d] with unit inner stride")
+    weight = weight.contiguous()
+    N, d = hidden.shape
+    V = weight.shape[0]
+    ids = ids.to(device=dev, dtype=torch.int64).contiguous()
+    grad_logp = grad_logp.to(device=dev, dtype=torch.float32).contiguous()
+    if grad_entropy is not None:
+        grad_entropy = grad_entropy.to(device=dev, dtype=torch.float32).contiguous()
+    if temperatures is not None:
+        temperatures = temperatures.to(device=dev, dtype=torch.float32).contiguous()
+    if ids.numel() != N or grad_logp.numel() != N or weight.shape[1] != d:
+        raise ValueError("shape mismatch")
+    dh = torch.empty(N, d, dtype=torch.float32, device=dev) if need_dhidden else None
+    dw = torch.empty(V, d, dtype=torch.float32, device=dev) if need_dweight else None
+    L = lib()
+    ws = _workspace(dev, L.tim_head_backward_workspace_bytes(N, d, V), "head_backward")
+    _check(L.tim_head_backward(_ptr(hidden), hidden.stride(0), _ptr(weight), d, V, _ptr(ids), N, float(temperature),
+                               _ptr(temperatures), _ptr(grad_logp), _ptr(grad_entropy), _ptr(dh), _ptr(dw), _ptr(ws),
+                               ws.numel(), _ptr(status), _stream(dev)), "tim_head_backward")
+    return dh, dw
 
 
 def debug_logits(hidden: torch.Tensor, weight: torch.Tensor, ids: torch.Tensor):

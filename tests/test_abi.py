@@ -76,6 +76,27 @@ def test_logprob_argument_errors_are_synchronous(L):
     assert _lp(L, wsb=100) == 5
 
 
+def _bw(L, hidden=P(4096), weight=P(8192), d=256, V=1024, ids=P(16), n=10, T=1.0, gl=P(32), dh=P(64),
+        dw=P(128), ws=P(1 << 20), wsb=1 << 40):
+    return L.tim_head_backward(hidden, 256, weight, d, V, ids, n, T, None, gl, None, dh, dw, ws, wsb, None, None)
+
+
+def test_head_backward_argument_errors_are_synchronous(L):
+    assert _bw(L, dh=None, dw=None) == 1
+    assert _bw(L, gl=None) == 1 and _bw(L, ids=None) == 1 and _bw(L, weight=None) == 1
+    assert _bw(L, d=200) == 2 and _bw(L, V=0) == 2 and _bw(L, n=-1) == 2
+    assert _bw(L, T=-1.0) == 4
+    assert _bw(L, dh=P(68)) == 3 and _bw(L, ws=P(4096 + 16)) == 3
+    assert _bw(L, wsb=1000) == 5
+    assert _bw(L, n=0, dw=None) == 0                   # empty batch, dhidden only: nothing to do
+    # workspace: forward partials + 3 per-token vectors + one bf16 G block of <= 4 GiB
+    nb = (1 << 32) // (2 * 151936) // 256 * 256
+    assert nb == 14080
+    assert L.tim_head_backward_workspace_bytes(100000, 2048, 151936) == \
+        (1024 + 8 * nb * 16) + 3 * nb * 4 + nb * 151936 * 2
+    assert L.tim_head_backward_workspace_bytes(1, 2048, 1000) == (1024 + 4 * 256 * 16) + 3 * 1024 + 256 * 1000 * 2
+
+
 def _cfg(**kw):
     c = tim.CorrectConfig(**kw).to_c()
     return c
