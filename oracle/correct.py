@@ -90,7 +90,8 @@ SMALL = 2.0 ** -6  # |delta| <= SMALL: short Horner polynomials (truncation < 1e
 
 
 def exp_contract(d) -> np.ndarray:
-    """C.3.6 exp_c.  |d| <= 2^-6: degree-7 Taylor Horner in d.  Otherwise Cody-Waite
+    """C.3.6 exp_c.  |d| <= 2^-6: (1 + d) + K3_small(d), K3_small = d^2 Q(d) the short
+    series of k3_contract (n = 2..9), i.e. e^d = 1 + d + (e^d - 1 - d).  Otherwise Cody-Waite
     reduction + degree-13 Taylor Horner + ldexp; +inf above 709, 0 below -700."""
     d = np.asarray(d, dtype=np.float64)
     dd = np.where(np.isfinite(d), np.clip(d, -700.0, 709.0), 0.0)
@@ -102,10 +103,10 @@ def exp_contract(d) -> np.ndarray:
     out = np.ldexp(p, k.astype(np.int64))
     small = np.abs(dd) <= SMALL
     ds = np.where(small, dd, 0.0)
-    q = np.full_like(ds, INV_FACT[7])
-    for n in range(6, -1, -1):
-        q = q * ds + INV_FACT[n]
-    out = np.where(small, q, out)
+    Q = np.full_like(ds, INV_FACT[9])
+    for n in range(8, 1, -1):
+        Q = Q * ds + INV_FACT[n]
+    out = np.where(small, (1.0 + ds) + (ds * ds) * Q, out)
     out = np.where(d > 709.0, np.inf, out)
     out = np.where(d < -700.0, 0.0, out)
     return out

@@ -30,17 +30,22 @@ constexpr long long kSatX = 1ll << 62;
 
 constexpr double kSmall = 0x1p-6;  // |d| <= 2^-6: short Horner polynomials
 
-// e^d.  |d| <= 2^-6: degree-7 Taylor (Horner) in d.  Otherwise Cody-Waite: k = rint(d log2 e),
-// r = (d - k ln2_hi) - k ln2_lo, degree-13 Taylor (Horner), * 2^k; +inf above 709, 0 below -700.
+// Short K3 series for |d| <= 2^-6: d^2 Q(d), Q = Horner of RN(1/n!), n = 2..9.
+__device__ __forceinline__ double k3_small(double d) {
+  double Q = kInvFact[9];
+#pragma unroll
+  for (int n = 8; n >= 2; --n) Q = __dadd_rn(__dmul_rn(Q, d), kInvFact[n]);
+  return __dmul_rn(__dmul_rn(d, d), Q);
+}
+
+// e^d.  |d| <= 2^-6: (1 + d) + k3_small(d) (e^d = 1 + d + K3, the K3 the caller needs anyway).
+// Otherwise Cody-Waite: k = rint(d log2 e), r = (d - k ln2_hi) - k ln2_lo, degree-13 Taylor
+// (Horner), * 2^k; +inf above 709, 0 below -700.
+__device__ __forceinline__ double exp_from_k3_small(double d, double k3s) { return __dadd_rn(__dadd_rn(1.0, d), k3s); }
 __device__ __forceinline__ double exp_c(double d) {
   if (d > 709.0) return CUDART_INF;
   if (d < -700.0) return 0.0;
-  if (fabs(d) <= kSmall) {
-    double q = kInvFact[7];
-#pragma unroll
-    for (int n = 6; n >= 0; --n) q = __dadd_rn(__dmul_rn(q, d), kInvFact[n]);
-    return q;
-  }
+  if (fabs(d) <= kSmall) return exp_from_k3_small(d, k3_small(d));
   const double k = rint(__dmul_rn(d, kLog2e));
   const double r = __dsub_rn(__dsub_rn(d, __dmul_rn(k, kLn2Hi)), __dmul_rn(k, kLn2Lo));
   double p = kInvFact[13];
@@ -51,15 +56,10 @@ __device__ __forceinline__ double exp_c(double d) {
 }
 
 // K3 = e^d - 1 - d = d^2 P(d): Horner series of (e^d - 1 - d) / d^2 with RN(1/n!), n = 2..9 for
-// |d| <= 2^-6, n = 2..23 for |d| <= 1; (exp_c(d) - 1) - d otherwise.
+// |d| <= 2^-6 (k3_small), n = 2..23 for |d| <= 1; (exp_c(d) - 1) - d otherwise.
 __device__ __forceinline__ double k3_c(double d) {
   const double ad = fabs(d);
-  if (ad <= kSmall) {
-    double Q = kInvFact[9];
-#pragma unroll
-    for (int n = 8; n >= 2; --n) Q = __dadd_rn(__dmul_rn(Q, d), kInvFact[n]);
-    return __dmul_rn(__dmul_rn(d, d), Q);
-  }
+  if (ad <= kSmall) return k3_small(d);
   if (ad <= 1.0) {
     double P = kInvFact[23];
 #pragma unroll

@@ -23,191 +23,241 @@
 
 namespace tim {
 
-#ifndef TIM_CORR_TPL
-#define TIM_CORR_TPL 4
-#endif
 #ifndef TIM_CORR_MINB
 #define TIM_CORR_MINB 3
 #endif
-constexpr int kTpl = TIM_CORR_TPL;      // tokens per lane
+constexpr int kTpl = 4;                 // tokens per lane (one float4 of num / den, one u32 of resp)
 constexpr int kWarpTok = 32 * kTpl;     // tokens per warp chunk
 constexpr int kLocalThreads = 256;
+constexpr int kFlushChunks = 4096;      // fast-path int64 sums are folded into int128 this often
 
-template <bool kOut, bool kSeq>
+// Per-thread rarely-touched state (int128 sums of the slow path, data errors), in shared memory
+// so the hot loop keeps its registers for the loads in flight and the Horner chains.
+struct SlowAcc {
+  __int128 s_abs, s_k1, s_k3, seq_x;
+  unsigned long long bad_inv;
+  long long c_sat, seq_nsat;
+  long long pad;
+};
+
+struct Chunk {
+  float4 num, den;
+  uint32_t resp;
+};
+
+__device__ __forceinline__ Chunk load_chunk(const LocalParams& p, long long i0) {
+  Chunk c;
+  if (i0 + kTpl <= p.n) {
+    c.num = __ldcs(reinterpret_cast<const float4*>(p.num + i0));
+    c.den = __ldcs(reinterpret_cast<const float4*>(p.den + i0));
+    c.resp = p.resp ? __ldcs(reinterpret_cast<const unsigned int*>(p.resp + i0)) : 0x01010101u;
+  } else {
+    float nv[4], dv[4];
+    uint32_t r = 0;
+#pragma unroll
+    for (int k = 0; k < kTpl; ++k) {
+      const long long i = i0 + k;
+      nv[k] = i < p.n ? p.num[i] : 0.f;
+      dv[k] = i < p.n ? p.den[i] : 0.f;
+      r |= static_cast<uint32_t>(i < p.n ? (p.resp ? (p.resp[i] != 0) : 1) : 0) << (8 * k);
+    }
+    c.num = make_float4(nv[0], nv[1], nv[2], nv[3]);
+    c.den = make_float4(dv[0], dv[1], dv[2], dv[3]);
+    c.resp = r;
+  }
+  return c;
+}
+
+// Pass 1 (a5).  Every warp owns a contiguous run of 128-token chunks (4 tokens per lane, the
+// next chunk's loads in flight while the current one computes).  Fast path, all lanes in
+// lockstep: tokens with |delta| <= 2^-6 (finite by construction) use the short contract
+// polynomials; their K values cannot saturate (|K| <= 2^-6), so they accumulate in int64
+// (|X| <= 2^46, folded into int128 every kFlushChunks chunks).  Slow path, per lane and rare:
+// larger or non-finite delta, a partial chunk, or a sequence boundary inside the lane's four
+// tokens -- the full per-token contract with int128 sums and the sequence walk.
+template <bool kOut, bool kSeq, bool kTis, bool kTokRs>
 __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_kernel(LocalParams p) {
+  __shared__ SlowAcc sh_slow[kLocalThreads];
   const int lane = threadIdx.x & 31;
   const long long warp_g = (static_cast<long long>(blockIdx.x) * kLocalThreads + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * kLocalThreads) >> 5;
   const long long n_chunks = (p.n + kWarpTok - 1) / kWarpTok;
   const CorrectDevCfg cfg = p.cfg;
+  SlowAcc& sa = sh_slow[threadIdx.x];
+  sa.s_abs = 0;
+  sa.s_k1 = 0;
+  sa.s_k3 = 0;
+  sa.seq_x = 0;
+  sa.bad_inv = 0;
+  sa.c_sat = 0;
+  sa.seq_nsat = 0;
 
-  long long c_resp = 0, c_trunc = 0, c_rej = 0, c_sat = 0;
-  __int128 s_abs = 0, s_k1 = 0, s_k3 = 0;
-  unsigned long long maxbits = 0;
-  unsigned long long bad_inv = 0;
+  unsigned c_resp = 0, c_trunc = 0, c_rej = 0;
+  long long f_abs = 0, f_k1 = 0, f_k3 = 0, f_seq = 0;  // fast-path exact sums
+  double mx = 0.0;                                     // max |delta| (finite response tokens)
+  long long seq_t = 0;
 
-  // every warp owns a contiguous run of chunks: one binary search per lane per run, then the
-  // per-lane sequence accumulator walks forward (flushing only when it crosses a boundary)
   const long long cpw = (n_chunks + nwarps - 1) / nwarps;
   const long long c_begin = warp_g * cpw;
   const long long c_end = c_begin + cpw < n_chunks ? c_begin + cpw : n_chunks;
-  SeqAcc acc;
-  acc.sid = LLONG_MAX;
-  acc.x = 0;
-  acc.t = 0;
-  acc.nsat = 0;
-  long long next_b = LLONG_MAX;
+  long long sid = LLONG_MAX, next_b = LLONG_MAX;
   if (kSeq && c_begin < c_end && c_begin * kWarpTok + lane * kTpl < p.n) {
-    acc.sid = seq_of(p.cu, p.n_seq, p.tok_begin + c_begin * kWarpTok + lane * kTpl);
-    next_b = __ldg(p.cu + acc.sid + 1);
+    sid = seq_of(p.cu, p.n_seq, p.tok_begin + c_begin * kWarpTok + lane * kTpl);
+    next_b = __ldg(p.cu + sid + 1);
   }
+  const bool seq_k1 = cfg.seq_rs == TIM_SEQ_K1;
+  const float cap_f = __double2float_rn(cfg.tis_cap);
 
+  Chunk nxt;
+  if (c_begin < c_end) nxt = load_chunk(p, c_begin * kWarpTok + lane * kTpl);
   for (long long ch = c_begin; ch < c_end; ++ch) {
     const long long i0 = ch * kWarpTok + lane * kTpl;
-    float num[kTpl], den[kTpl];
-    uint8_t rs[kTpl];
-    const bool full = (kTpl % 4 == 0) && i0 + kTpl <= p.n;  // vector path needs whole float4s
-    if (full) {
-#pragma unroll
-      for (int v = 0; v < kTpl / 4; ++v) {
-        const float4 a = __ldg(reinterpret_cast<const float4*>(p.num + i0) + v);
-        const float4 b = __ldg(reinterpret_cast<const float4*>(p.den + i0) + v);
-        num[4 * v] = a.x; num[4 * v + 1] = a.y; num[4 * v + 2] = a.z; num[4 * v + 3] = a.w;
-        den[4 * v] = b.x; den[4 * v + 1] = b.y; den[4 * v + 2] = b.z; den[4 * v + 3] = b.w;
-      }
-      if (p.resp) {
-#pragma unroll
-        for (int v = 0; v < kTpl / 4; ++v) {
-          const uint32_t m = __ldg(reinterpret_cast<const uint32_t*>(p.resp + i0) + v);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) rs[4 * v + k] = (m >> (8 * k)) & 0xff;
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < kTpl; ++k) rs[k] = 1;
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < kTpl; ++k) {
-        const long long i = i0 + k;
-        num[k] = i < p.n ? p.num[i] : 0.f;
-        den[k] = i < p.n ? p.den[i] : 0.f;
-        rs[k] = i < p.n ? (p.resp ? p.resp[i] : 1) : 0;
-      }
-    }
+    const Chunk cur = nxt;
+    if (ch + 1 < c_end) nxt = load_chunk(p, i0 + kWarpTok);
+    const float num[4] = {cur.num.x, cur.num.y, cur.num.z, cur.num.w};
+    const float den[4] = {cur.den.x, cur.den.y, cur.den.z, cur.den.w};
 
-    // (1) delta for the lane's 8 tokens; (2) the short small-|delta| polynomials of all 8 tokens in
-    // lockstep (8 independent Horner chains: latency hidden by ILP); (3) the rare tokens outside
-    // [-2^-6, 2^-6] take the long contract paths.  Same op sequence per token as exp_c / k3_c.
-    double dv[kTpl], ds[kTpl], ev[kTpl], k3v[kTpl];
-    unsigned big_mask = 0;
+    double dv[kTpl], ds[kTpl], k3s[kTpl];
+    unsigned slow = i0 + kTpl <= p.n ? 0u : 0xFu;
+    if (kSeq && p.tok_begin + i0 + (kTpl - 1) >= next_b) slow = 0xFu;
 #pragma unroll
     for (int k = 0; k < kTpl; ++k) {
       dv[k] = __dsub_rn(static_cast<double>(num[k]), static_cast<double>(den[k]));
-      const bool ok = i0 + k < p.n && isfinite(dv[k]);
-      const bool sm = ok && fabs(dv[k]) <= kSmall;
-      if (ok && !sm) big_mask |= 1u << k;
+      const bool sm = fabs(dv[k]) <= kSmall;  // false for NaN / inf
+      if (!sm) slow |= 1u << k;
       ds[k] = sm ? dv[k] : 0.0;
-      k3v[k] = kInvFact[9];
-      ev[k] = kInvFact[7];
     }
+    // short K3 series of the four tokens in lockstep (independent Horner chains)
+    double q[kTpl];
+#pragma unroll
+    for (int k = 0; k < kTpl; ++k) q[k] = kInvFact[9];
 #pragma unroll
     for (int n = 8; n >= 2; --n)
 #pragma unroll
-      for (int k = 0; k < kTpl; ++k) k3v[k] = __dadd_rn(__dmul_rn(k3v[k], ds[k]), kInvFact[n]);
+      for (int k = 0; k < kTpl; ++k) q[k] = __dadd_rn(__dmul_rn(q[k], ds[k]), kInvFact[n]);
 #pragma unroll
-    for (int k = 0; k < kTpl; ++k) k3v[k] = __dmul_rn(__dmul_rn(ds[k], ds[k]), k3v[k]);
-    if (cfg.tis) {
-#pragma unroll
-      for (int n = 6; n >= 0; --n)
-#pragma unroll
-        for (int k = 0; k < kTpl; ++k) ev[k] = __dadd_rn(__dmul_rn(ev[k], ds[k]), kInvFact[n]);
-    }
-    if (big_mask) {
-#pragma unroll
-      for (int k = 0; k < kTpl; ++k) {
-        if ((big_mask >> k) & 1u) {
-          k3v[k] = k3_c(dv[k]);
-          if (cfg.tis) ev[k] = exp_c(dv[k]);
-        }
-      }
-    }
+    for (int k = 0; k < kTpl; ++k) k3s[k] = __dmul_rn(__dmul_rn(ds[k], ds[k]), q[k]);
 
     float w_out[kTpl], c_out[kTpl];
-    uint8_t k_out[kTpl];
+    uint32_t kbits = 0;
+    // this chunk's exact sums in fp64: every X is an integer with |X| <= 2^46, so the sums of
+    // four are exact doubles; one conversion per sum per chunk
+    double ck1 = 0.0, ck3 = 0.0, cabs = 0.0, cseq = 0.0, cmx = 0.0;
+    unsigned cn = 0, ctr = 0, crj = 0, cst = 0;
 #pragma unroll
     for (int k = 0; k < kTpl; ++k) {
-      const long long i = i0 + k;
-      w_out[k] = 1.f;
-      c_out[k] = 0.f;
-      k_out[k] = 1;
-      if (i >= p.n) continue;
-      const long long g = p.tok_begin + i;
-      const double d = dv[k];
-      if (!isfinite(d)) {  // C.3.2 data error: excluded from every sum, outputs NaN / 0
-        const unsigned long long b = kBadSentinel - static_cast<unsigned long long>(g);
-        bad_inv = b > bad_inv ? b : bad_inv;
-        w_out[k] = CUDART_NAN_F;
-        k_out[k] = 0;
-        continue;
+      const double d = ds[k];
+      const bool resp = (cur.resp >> (8 * k)) & 0xffu;
+      const bool use = resp && !((slow >> k) & 1u);
+      bool trunc = false;
+      float w = 1.f;
+      if (kTis) {  // (float) min(e, cap) == min((float) e, (float) cap): rounding is monotonic
+        trunc = d > cfg.log_tis_cap;
+        w = trunc ? cap_f : fminf(__double2float_rn(exp_from_k3_small(d, k3s[k])), cap_f);
       }
-      const bool resp = rs[k] != 0;
-      const bool trunc = cfg.tis && d > cfg.log_tis_cap;
-      if (cfg.tis) {
-        const double w = trunc ? cfg.tis_cap : fmin(ev[k], cfg.tis_cap);
-        w_out[k] = __double2float_rn(w);
-      }
-      const bool keep = cfg.tok_rs ? (cfg.log_lo <= d && d <= cfg.log_hi) : true;
-      k_out[k] = keep ? 1 : 0;
-      c_out[k] = (resp && keep) ? w_out[k] : 0.f;
-
-      bool sat1, sat3;
-      const long long x1 = fixed_point(-d, sat1);
-      const double k3 = k3v[k];
-      const long long x3 = fixed_point(k3, sat3);
-      if (resp) {
-        // rint is odd-symmetric and |K1| = |delta| saturate together: X(|delta|) = |X(-delta)|
-        const long long xa = x1 < 0 ? -x1 : x1;
-        c_resp += 1;
-        c_trunc += trunc ? 1 : 0;
-        c_rej += keep ? 0 : 1;
-        s_abs += xa;
-        s_k1 += x1;
-        s_k3 += x3;
-        const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(fabs(d)));
-        maxbits = bits > maxbits ? bits : maxbits;
-      }
+      const bool keep = kTokRs ? (cfg.log_lo <= d && d <= cfg.log_hi) : true;
+      w_out[k] = w;
+      c_out[k] = (resp && keep) ? w : 0.f;
+      kbits |= static_cast<uint32_t>(keep) << (8 * k);
+      const double dz = use ? d : 0.0;  // unused tokens contribute exactly 0 to every sum
+      const double kz = use ? k3s[k] : 0.0;
+      const double x1 = rint(__dmul_rn(-dz, kTwo52));  // exact scaling, then round to integer
+      const double x3 = rint(__dmul_rn(kz, kTwo52));
+      ck1 = __dadd_rn(ck1, x1);
+      ck3 = __dadd_rn(ck3, x3);
+      cabs = __dadd_rn(cabs, fabs(x1));
+      const double ad = fabs(dz);
+      cmx = ad > cmx ? ad : cmx;
+      cn += use ? 1u : 0u;
+      if (kTis) ctr += (use && trunc) ? 1u : 0u;
+      if (kTokRs) crj += (use && !keep) ? 1u : 0u;
       if (kSeq) {
-        while (g >= next_b) {  // crossed into a later sequence (skips empty ones)
-          flush_seq(p.seqp, acc);
-          acc.x = 0;
-          acc.t = 0;
-          acc.nsat = 0;
-          acc.sid += 1;
-          next_b = __ldg(p.cu + acc.sid + 1);
+        if (kTokRs) cseq = __dadd_rn(cseq, keep ? (seq_k1 ? x1 : x3) : 0.0);
+        cst += (use && keep) ? 1u : 0u;
+      }
+    }
+    const long long ik1 = __double2ll_rn(ck1), ik3 = __double2ll_rn(ck3);
+    f_k1 += ik1;
+    f_k3 += ik3;
+    f_abs += __double2ll_rn(cabs);
+    mx = cmx > mx ? cmx : mx;
+    c_resp += cn;
+    c_trunc += ctr;
+    c_rej += crj;
+    if (kSeq) {
+      f_seq += kTokRs ? __double2ll_rn(cseq) : (seq_k1 ? ik1 : ik3);
+      seq_t += cst;
+    }
+
+    if (slow) {  // rare: the full contract per token, in the slow tokens' lanes only
+#pragma unroll
+      for (int k = 0; k < kTpl; ++k) {
+        if (!((slow >> k) & 1u)) continue;
+        const long long i = i0 + k;
+        if (i >= p.n) continue;
+        const long long g = p.tok_begin + i;
+        const double d = dv[k];
+        if (kSeq) {
+          while (g >= next_b) {  // crossed into a later sequence (skips empty ones)
+            SeqAcc a;
+            a.sid = sid;
+            a.x = sa.seq_x + static_cast<__int128>(f_seq);
+            a.t = seq_t;
+            a.nsat = sa.seq_nsat;
+            flush_seq(p.seqp, a);
+            sa.seq_x = 0;
+            sa.seq_nsat = 0;
+            f_seq = 0;
+            seq_t = 0;
+            sid += 1;
+            next_b = __ldg(p.cu + sid + 1);
+          }
         }
-        if (resp && keep) {
-          const bool satq = cfg.seq_rs == TIM_SEQ_K1 ? sat1 : sat3;
-          acc.x += cfg.seq_rs == TIM_SEQ_K1 ? x1 : x3;
-          acc.t += 1;
-          acc.nsat += satq ? 1 : 0;
-          c_sat += satq ? 1 : 0;
+        if (!isfinite(d)) {  // C.3.2 data error: excluded from every sum, outputs NaN / 0
+          const unsigned long long b = kBadSentinel - static_cast<unsigned long long>(g);
+          sa.bad_inv = b > sa.bad_inv ? b : sa.bad_inv;
+          w_out[k] = CUDART_NAN_F;
+          c_out[k] = 0.f;
+          kbits &= ~(0xffu << (8 * k));
+          continue;
+        }
+        const bool resp = (cur.resp >> (8 * k)) & 0xffu;
+        const bool sm = fabs(d) <= kSmall;
+        const double k3 = sm ? k3s[k] : k3_c(d);
+        const bool trunc = kTis && d > cfg.log_tis_cap;
+        if (kTis) {
+          const double e = sm ? exp_from_k3_small(d, k3) : exp_c(d);
+          w_out[k] = __double2float_rn(trunc ? cfg.tis_cap : fmin(e, cfg.tis_cap));
+        }
+        const bool keep = kTokRs ? (cfg.log_lo <= d && d <= cfg.log_hi) : true;
+        c_out[k] = (resp && keep) ? w_out[k] : 0.f;
+        kbits = (kbits & ~(0xffu << (8 * k))) | (static_cast<uint32_t>(keep) << (8 * k));
+        if (!resp) continue;
+        bool sat1, sat3;
+        const long long x1 = fixed_point(-d, sat1);
+        const long long x3 = fixed_point(k3, sat3);
+        c_resp += 1;
+        c_trunc += trunc ? 1u : 0u;
+        c_rej += keep ? 0u : 1u;
+        sa.s_abs += x1 < 0 ? -x1 : x1;  // rint is odd-symmetric: X(|delta|) = |X(-delta)|
+        sa.s_k1 += x1;
+        sa.s_k3 += x3;
+        mx = fmax(mx, fabs(d));
+        if (kSeq && keep) {
+          const bool satq = seq_k1 ? sat1 : sat3;
+          sa.seq_x += seq_k1 ? x1 : x3;
+          seq_t += 1;
+          sa.seq_nsat += satq ? 1 : 0;
+          sa.c_sat += satq ? 1 : 0;
         }
       }
     }
 
     if (kOut) {
-      if (full) {
-        float4* pw = reinterpret_cast<float4*>(p.tis_w + i0);
-        float4* pc = reinterpret_cast<float4*>(p.coeff + i0);
-#pragma unroll
-        for (int v = 0; v < kTpl / 4; ++v) {
-          pw[v] = make_float4(w_out[4 * v], w_out[4 * v + 1], w_out[4 * v + 2], w_out[4 * v + 3]);
-          pc[v] = make_float4(c_out[4 * v], c_out[4 * v + 1], c_out[4 * v + 2], c_out[4 * v + 3]);
-          reinterpret_cast<uint32_t*>(p.tok_keep + i0)[v] =
-              k_out[4 * v] | (k_out[4 * v + 1] << 8) | (k_out[4 * v + 2] << 16) |
-              (static_cast<uint32_t>(k_out[4 * v + 3]) << 24);
-        }
+      if (i0 + kTpl <= p.n) {
+        __stcs(reinterpret_cast<float4*>(p.tis_w + i0), make_float4(w_out[0], w_out[1], w_out[2], w_out[3]));
+        __stcs(reinterpret_cast<float4*>(p.coeff + i0), make_float4(c_out[0], c_out[1], c_out[2], c_out[3]));
+        __stcs(reinterpret_cast<unsigned int*>(p.tok_keep + i0), kbits);
       } else {
 #pragma unroll
         for (int k = 0; k < kTpl; ++k) {
@@ -215,15 +265,31 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
           if (i < p.n) {
             p.tis_w[i] = w_out[k];
             p.coeff[i] = c_out[k];
-            p.tok_keep[i] = k_out[k];
+            p.tok_keep[i] = (kbits >> (8 * k)) & 0xffu;
           }
         }
       }
     }
-
+    if (((ch - c_begin) & (kFlushChunks - 1)) == kFlushChunks - 1) {
+      sa.s_abs += f_abs;
+      sa.s_k1 += f_k1;
+      sa.s_k3 += f_k3;
+      sa.seq_x += f_seq;
+      f_abs = f_k1 = f_k3 = f_seq = 0;
+    }
   }
 
+  __int128 s_abs = sa.s_abs + f_abs, s_k1 = sa.s_k1 + f_k1, s_k3 = sa.s_k3 + f_k3;
+  unsigned long long maxbits = static_cast<unsigned long long>(__double_as_longlong(mx));
+  unsigned long long bad_inv = sa.bad_inv;
+  long long c_sat = sa.c_sat;
+
   if (kSeq) {
+    SeqAcc acc;
+    acc.sid = sid;
+    acc.x = sa.seq_x + static_cast<__int128>(f_seq);
+    acc.t = seq_t;
+    acc.nsat = sa.seq_nsat;
     // segmented warp reduction of the open segments (sequence ids are non-decreasing in lane order)
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -237,8 +303,8 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
         acc.nsat += on;
       }
     }
-    // note: lane l now holds the sum of lanes [l, l+2^k) with the same id, so the head of each
-    // run (first lane of that id) holds the whole run because runs are contiguous.
+    // lane l now holds the sum of lanes [l, l+2^k) with the same id, so the head of each run
+    // (first lane of that id) holds the whole run because runs are contiguous.
     const long long prev_sid = __shfl_up_sync(0xffffffffu, acc.sid, 1);
     const bool head = lane == 0 || prev_sid != acc.sid;
     if (head && acc.sid != LLONG_MAX) flush_seq(p.seqp, acc);
@@ -249,9 +315,9 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
   __shared__ long long sh_sum[6][kLocalThreads / 32];
   __shared__ unsigned long long sh_max[kLocalThreads / 32], sh_bad[kLocalThreads / 32];
   const int w = threadIdx.x >> 5;
-  c_resp = warp_sum_i64(c_resp);
-  c_trunc = warp_sum_i64(c_trunc);
-  c_rej = warp_sum_i64(c_rej);
+  const long long n_resp = warp_sum_i64(static_cast<long long>(c_resp));
+  const long long n_trunc = warp_sum_i64(static_cast<long long>(c_trunc));
+  const long long n_rej = warp_sum_i64(static_cast<long long>(c_rej));
   c_sat = warp_sum_i64(c_sat);
   s_abs = warp_sum_i128(s_abs);
   s_k1 = warp_sum_i128(s_k1);
@@ -259,9 +325,9 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
   maxbits = warp_max_u64(maxbits);
   bad_inv = warp_max_u64(bad_inv);
   if (lane == 0) {
-    sh_cnt[0][w] = c_resp;
-    sh_cnt[1][w] = c_trunc;
-    sh_cnt[2][w] = c_rej;
+    sh_cnt[0][w] = n_resp;
+    sh_cnt[1][w] = n_trunc;
+    sh_cnt[2][w] = n_rej;
     sh_cnt[3][w] = c_sat;
     sh_sum[0][w] = static_cast<long long>(static_cast<unsigned long long>(s_abs));
     sh_sum[1][w] = static_cast<long long>(s_abs >> 64);
@@ -276,13 +342,13 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
   if (threadIdx.x == 0) {
     long long cnt[4] = {0, 0, 0, 0};
     __int128 sums[3] = {0, 0, 0};
-    unsigned long long mx = 0, bd = 0;
+    unsigned long long mxb = 0, bd = 0;
     for (int i = 0; i < kLocalThreads / 32; ++i) {
       for (int k = 0; k < 4; ++k) cnt[k] += sh_cnt[k][i];
       for (int k = 0; k < 3; ++k)
         sums[k] += (static_cast<__int128>(sh_sum[2 * k + 1][i]) << 64) |
                    static_cast<__int128>(static_cast<unsigned long long>(sh_sum[2 * k][i]));
-      mx = sh_max[i] > mx ? sh_max[i] : mx;
+      mxb = sh_max[i] > mxb ? sh_max[i] : mxb;
       bd = sh_bad[i] > bd ? sh_bad[i] : bd;
     }
     tim_partial_header* h = p.hdr;
@@ -295,7 +361,7 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
     atomic_add_i128(h->sum_abs_delta, sums[0]);
     atomic_add_i128(h->sum_k1, sums[1]);
     atomic_add_i128(h->sum_k3, sums[2]);
-    if (mx) atomicMax(reinterpret_cast<unsigned long long*>(&h->max_abs_delta_bits), mx);
+    if (mxb) atomicMax(reinterpret_cast<unsigned long long*>(&h->max_abs_delta_bits), mxb);
     if (bd) atomicMax(reinterpret_cast<unsigned long long*>(&h->reserved[0]), bd);
   }
   // status commit by the last block (ticket in hdr->reserved[1], bad index in reserved[0])
@@ -394,10 +460,21 @@ cudaError_t launch_correct_local(const LocalParams& p, int num_sms, cudaStream_t
   if (blocks < 1) blocks = 1;
   const bool out = p.tis_w != nullptr;
   const bool seq = p.cfg.seq_rs != TIM_SEQ_NONE;
-  if (out && seq) correct_local_kernel<true, true><<<blocks, kLocalThreads, 0, stream>>>(p);
-  else if (out) correct_local_kernel<true, false><<<blocks, kLocalThreads, 0, stream>>>(p);
-  else if (seq) correct_local_kernel<false, true><<<blocks, kLocalThreads, 0, stream>>>(p);
-  else correct_local_kernel<false, false><<<blocks, kLocalThreads, 0, stream>>>(p);
+  const int v = (out ? 8 : 0) | (seq ? 4 : 0) | (p.cfg.tis ? 2 : 0) | (p.cfg.tok_rs ? 1 : 0);
+  switch (v) {
+#define TIM_CORR_CASE(o, s, t, r) \
+  case (o ? 8 : 0) | (s ? 4 : 0) | (t ? 2 : 0) | (r ? 1 : 0): \
+    correct_local_kernel<o, s, t, r><<<blocks, kLocalThreads, 0, stream>>>(p); break;
+    TIM_CORR_CASE(true, true, true, true) TIM_CORR_CASE(true, true, true, false)
+    TIM_CORR_CASE(true, true, false, true) TIM_CORR_CASE(true, true, false, false)
+    TIM_CORR_CASE(true, false, true, true) TIM_CORR_CASE(true, false, true, false)
+    TIM_CORR_CASE(true, false, false, true) TIM_CORR_CASE(true, false, false, false)
+    TIM_CORR_CASE(false, true, true, true) TIM_CORR_CASE(false, true, true, false)
+    TIM_CORR_CASE(false, true, false, true) TIM_CORR_CASE(false, true, false, false)
+    TIM_CORR_CASE(false, false, true, true) TIM_CORR_CASE(false, false, true, false)
+    TIM_CORR_CASE(false, false, false, true) TIM_CORR_CASE(false, false, false, false)
+#undef TIM_CORR_CASE
+  }
   return cudaGetLastError();
 }
 

@@ -77,10 +77,7 @@ __global__ void __launch_bounds__(kPpoThreads, 2) ppo_local_kernel(PpoLocalParam
       const bool sm = ok && fabs(dv[k]) <= kSmall;
       if (ok && !sm) big_mask |= 1u << k;
       const double ds = sm ? dv[k] : 0.0;
-      double q = kInvFact[7];
-#pragma unroll
-      for (int n = 6; n >= 0; --n) q = __dadd_rn(__dmul_rn(q, ds), kInvFact[n]);
-      rv[k] = q;
+      rv[k] = exp_from_k3_small(ds, k3_small(ds));
     }
     if (big_mask) {
 #pragma unroll
