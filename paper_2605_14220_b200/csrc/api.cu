@@ -918,6 +918,8 @@ tim_status tim_ppo_local(const float* cur, const float* old, const float* adv, c
   p.seqp = reinterpret_cast<tim_seq_partial*>(blk + sizeof(tim_ppo_partial_header) +
                                               16u * static_cast<size_t>(cfg->hist_bins + 2));
   p.dstatus = dstatus;
+  p.vec = aligned(adv, 16) && aligned(coeff, 16) && aligned(loss, 16) && aligned(grad, 16) && aligned(clipped, 4) &&
+          aligned(resp, 4);
   return launch_ppo_local(p, dev->num_sms, s) == cudaSuccess ? TIM_OK : TIM_ERR_CUDA;
 }
 

@@ -38,14 +38,17 @@ __device__ __forceinline__ double k3_small(double d) {
   return __dmul_rn(__dmul_rn(d, d), Q);
 }
 
-// e^d.  |d| <= 2^-6: (1 + d) + k3_small(d) (e^d = 1 + d + K3, the K3 the caller needs anyway).
-// Otherwise Cody-Waite: k = rint(d log2 e), r = (d - k ln2_hi) - k ln2_lo, degree-13 Taylor
-// (Horner), * 2^k; +inf above 709, 0 below -700.
-__device__ __forceinline__ double exp_from_k3_small(double d, double k3s) { return __dadd_rn(__dadd_rn(1.0, d), k3s); }
-__device__ __forceinline__ double exp_c(double d) {
-  if (d > 709.0) return CUDART_INF;
-  if (d < -700.0) return 0.0;
-  if (fabs(d) <= kSmall) return exp_from_k3_small(d, k3_small(d));
+// Medium K3 series for |d| <= 1: d^2 P(d), P = Horner of RN(1/n!), n = 2..23.
+__device__ __forceinline__ double k3_medium(double d) {
+  double P = kInvFact[23];
+#pragma unroll
+  for (int n = 22; n >= 2; --n) P = __dadd_rn(__dmul_rn(P, d), kInvFact[n]);
+  return __dmul_rn(__dmul_rn(d, d), P);
+}
+
+// Cody-Waite e^d for -700 <= d <= 709: k = rint(d log2 e), r = (d - k ln2_hi) - k ln2_lo,
+// degree-13 Taylor (Horner), * 2^k.
+__device__ __forceinline__ double exp_cw(double d) {
   const double k = rint(__dmul_rn(d, kLog2e));
   const double r = __dsub_rn(__dsub_rn(d, __dmul_rn(k, kLn2Hi)), __dmul_rn(k, kLn2Lo));
   double p = kInvFact[13];
@@ -55,17 +58,22 @@ __device__ __forceinline__ double exp_c(double d) {
   return __dmul_rn(p, __longlong_as_double((ki + 1023) << 52));
 }
 
+// e^d.  |d| <= 2^-6: (1 + d) + k3_small(d) (e^d = 1 + d + K3, the K3 the caller needs anyway).
+// Otherwise Cody-Waite (exp_cw); +inf above 709, 0 below -700.
+__device__ __forceinline__ double exp_from_k3_small(double d, double k3s) { return __dadd_rn(__dadd_rn(1.0, d), k3s); }
+__device__ __forceinline__ double exp_c(double d) {
+  if (d > 709.0) return CUDART_INF;
+  if (d < -700.0) return 0.0;
+  if (fabs(d) <= kSmall) return exp_from_k3_small(d, k3_small(d));
+  return exp_cw(d);
+}
+
 // K3 = e^d - 1 - d = d^2 P(d): Horner series of (e^d - 1 - d) / d^2 with RN(1/n!), n = 2..9 for
-// |d| <= 2^-6 (k3_small), n = 2..23 for |d| <= 1; (exp_c(d) - 1) - d otherwise.
+// |d| <= 2^-6 (k3_small), n = 2..23 for |d| <= 1 (k3_medium); (exp_c(d) - 1) - d otherwise.
 __device__ __forceinline__ double k3_c(double d) {
   const double ad = fabs(d);
   if (ad <= kSmall) return k3_small(d);
-  if (ad <= 1.0) {
-    double P = kInvFact[23];
-#pragma unroll
-    for (int n = 22; n >= 2; --n) P = __dadd_rn(__dmul_rn(P, d), kInvFact[n]);
-    return __dmul_rn(__dmul_rn(d, d), P);
-  }
+  if (ad <= 1.0) return k3_medium(d);
   return __dsub_rn(__dsub_rn(exp_c(d), 1.0), d);
 }
 

@@ -18,12 +18,63 @@
 
 namespace tim {
 
-constexpr int kPpoTpl = 8;
+constexpr int kPpoTpl = 4;                  // tokens per lane: one float4 of each input
 constexpr int kPpoWarpTok = 32 * kPpoTpl;
 constexpr int kPpoThreads = 256;
+constexpr int kPpoMinB = 2;
 constexpr int kMaxHistBins = 1024;
+constexpr double kPpoFastLoss = 256.0;      // fast path: |loss| <= 2^8, so |X| <= 2^60 and four fit int64
 
-__global__ void __launch_bounds__(kPpoThreads, 2) ppo_local_kernel(PpoLocalParams p) {
+struct PpoChunk {
+  float4 cur, old, adv, w;  // w = coeff, or the response mask as 0 / 1
+};
+
+__device__ __forceinline__ PpoChunk ppo_load(const PpoLocalParams& p, long long i0) {
+  PpoChunk c;
+  if (p.vec && i0 + kPpoTpl <= p.n) {
+    c.cur = __ldcs(reinterpret_cast<const float4*>(p.cur + i0));
+    c.old = __ldcs(reinterpret_cast<const float4*>(p.old + i0));
+    c.adv = __ldcs(reinterpret_cast<const float4*>(p.adv + i0));
+    if (p.coeff) {
+      c.w = __ldcs(reinterpret_cast<const float4*>(p.coeff + i0));
+    } else if (p.resp) {
+      const uint32_t m = __ldcs(reinterpret_cast<const unsigned int*>(p.resp + i0));
+      c.w = make_float4((m & 0xffu) ? 1.f : 0.f, (m & 0xff00u) ? 1.f : 0.f, (m & 0xff0000u) ? 1.f : 0.f,
+                        (m & 0xff000000u) ? 1.f : 0.f);
+    } else {
+      c.w = make_float4(1.f, 1.f, 1.f, 1.f);
+    }
+  } else {
+    float v[4][4];
+#pragma unroll
+    for (int k = 0; k < kPpoTpl; ++k) {
+      const long long i = i0 + k;
+      const bool in = i < p.n;
+      v[0][k] = in ? p.cur[i] : 0.f;
+      v[1][k] = in ? p.old[i] : 0.f;
+      v[2][k] = in ? p.adv[i] : 0.f;
+      v[3][k] = !in ? 0.f : (p.coeff ? p.coeff[i] : ((p.resp ? p.resp[i] != 0 : true) ? 1.f : 0.f));
+    }
+    c.cur = make_float4(v[0][0], v[0][1], v[0][2], v[0][3]);
+    c.old = make_float4(v[1][0], v[1][1], v[1][2], v[1][3]);
+    c.adv = make_float4(v[2][0], v[2][1], v[2][2], v[2][3]);
+    c.w = make_float4(v[3][0], v[3][1], v[3][2], v[3][3]);
+  }
+  return c;
+}
+
+__device__ __forceinline__ int hist_slot(const PpoLocalParams& p, double r, double A) {
+  const double C = __dmul_rn(-__dsub_rn(r, 1.0), A);
+  const double raw = floor(__dmul_rn(__dsub_rn(C, p.hist_lo), p.hist_inv_width));
+  return raw < 0.0 ? 0 : (raw >= static_cast<double>(p.bins) ? p.bins + 1 : static_cast<int>(raw) + 1);
+}
+
+// Same structure as correct_local_kernel: 4 tokens per lane, next chunk prefetched, a lock-step
+// fast path (|delta| <= 1, |loss| <= 2^8: contract polynomials in lock-step, exact int64 chunk
+// sums folded into int128 per chunk) and a rare per-lane slow path with the full contract
+// (larger delta or loss, non-finite input, partial or unaligned chunk, sequence boundary inside
+// the lane's tokens).
+__global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLocalParams p) {
   extern __shared__ int sh_hist[];  // [2][bins + 2]
   const int nslot = p.bins + 2;
   for (int i = threadIdx.x; i < 2 * nslot; i += blockDim.x) sh_hist[i] = 0;
@@ -37,7 +88,7 @@ __global__ void __launch_bounds__(kPpoThreads, 2) ppo_local_kernel(PpoLocalParam
   const long long c_begin = warp_g * cpw;
   const long long c_end = c_begin + cpw < n_chunks ? c_begin + cpw : n_chunks;
 
-  long long c_contrib = 0, c_clip = 0, c_zero = 0, c_sat = 0;
+  unsigned c_contrib = 0, c_clip = 0, c_zero = 0, c_sat = 0;
   __int128 s_loss = 0, s_k1 = 0, s_k3 = 0;
   unsigned long long bad_inv = 0;
 
@@ -52,95 +103,166 @@ __global__ void __launch_bounds__(kPpoThreads, 2) ppo_local_kernel(PpoLocalParam
     next_b = __ldg(p.cu + acc.sid + 1);
   }
 
+  PpoChunk nxt;
+  if (c_begin < c_end) nxt = ppo_load(p, c_begin * kPpoWarpTok + lane * kPpoTpl);
   for (long long ch = c_begin; ch < c_end; ++ch) {
     const long long i0 = ch * kPpoWarpTok + lane * kPpoTpl;
-    double dv[kPpoTpl], rv[kPpoTpl];
-    float adv[kPpoTpl], wv[kPpoTpl];
-    bool cb[kPpoTpl];
-    unsigned big_mask = 0;
+    const PpoChunk cur = nxt;
+    if (ch + 1 < c_end) nxt = ppo_load(p, i0 + kPpoWarpTok);
+    const float cu_[4] = {cur.cur.x, cur.cur.y, cur.cur.z, cur.cur.w};
+    const float ol_[4] = {cur.old.x, cur.old.y, cur.old.z, cur.old.w};
+    const float ad_[4] = {cur.adv.x, cur.adv.y, cur.adv.z, cur.adv.w};
+    const float wv_[4] = {cur.w.x, cur.w.y, cur.w.z, cur.w.w};
+    const bool full = p.vec && i0 + kPpoTpl <= p.n;
+
+    // fast tokens: |delta| <= 1 (finite).  The short (|delta| <= 2^-6) and the medium contract
+    // branches both run in lock-step over the lane's four tokens (the medium one only when some
+    // lane of the warp needs it), each token then takes its branch's value.
+    double dv[kPpoTpl], ds[kPpoTpl], dm[kPpoTpl], k3s[kPpoTpl], k3m[kPpoTpl], em[kPpoTpl];
+    unsigned slow = full ? 0u : 0xFu;
+    if (p.tok_begin + i0 + (kPpoTpl - 1) >= next_b) slow = 0xFu;
+    bool any_med = false;
 #pragma unroll
     for (int k = 0; k < kPpoTpl; ++k) {
-      const long long i = i0 + k;
-      const bool in = i < p.n;
-      const float cur = in ? __ldg(p.cur + i) : 0.f;
-      const float old = in ? __ldg(p.old + i) : 0.f;
-      adv[k] = in ? __ldg(p.adv + i) : 0.f;
-      if (p.coeff) {
-        wv[k] = in ? __ldg(p.coeff + i) : 0.f;
-        cb[k] = wv[k] != 0.f;
-      } else {
-        cb[k] = in && (p.resp ? __ldg(p.resp + i) != 0 : true);
-        wv[k] = cb[k] ? 1.f : 0.f;
-      }
-      dv[k] = __dsub_rn(static_cast<double>(cur), static_cast<double>(old));
-      const bool ok = in && isfinite(dv[k]);
-      const bool sm = ok && fabs(dv[k]) <= kSmall;
-      if (ok && !sm) big_mask |= 1u << k;
-      const double ds = sm ? dv[k] : 0.0;
-      rv[k] = exp_from_k3_small(ds, k3_small(ds));
+      dv[k] = __dsub_rn(static_cast<double>(cu_[k]), static_cast<double>(ol_[k]));
+      const double ad = fabs(dv[k]);
+      const bool tiny = ad <= kSmall;  // false for NaN / inf
+      const bool med = !tiny && ad <= 1.0;
+      if (!tiny && !med) slow |= 1u << k;
+      ds[k] = tiny ? dv[k] : 0.0;
+      dm[k] = med ? dv[k] : 0.0;
+      any_med = any_med || med;
     }
-    if (big_mask) {
+    double q[kPpoTpl];
 #pragma unroll
-      for (int k = 0; k < kPpoTpl; ++k)
-        if ((big_mask >> k) & 1u) rv[k] = exp_c(dv[k]);
+    for (int k = 0; k < kPpoTpl; ++k) q[k] = kInvFact[9];
+#pragma unroll
+    for (int n = 8; n >= 2; --n)
+#pragma unroll
+      for (int k = 0; k < kPpoTpl; ++k) q[k] = __dadd_rn(__dmul_rn(q[k], ds[k]), kInvFact[n]);
+#pragma unroll
+    for (int k = 0; k < kPpoTpl; ++k) k3s[k] = __dmul_rn(__dmul_rn(ds[k], ds[k]), q[k]);
+    if (__any_sync(0xffffffffu, any_med)) {
+#pragma unroll
+      for (int k = 0; k < kPpoTpl; ++k) k3m[k] = k3_medium(dm[k]);
+#pragma unroll
+      for (int k = 0; k < kPpoTpl; ++k) em[k] = exp_cw(dm[k]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kPpoTpl; ++k) {
+        k3m[k] = 0.0;
+        em[k] = 1.0;
+      }
     }
 
+    float l_out[kPpoTpl], g_out[kPpoTpl];
+    uint32_t cbits = 0;
+    long long cl = 0, ck1 = 0, ck3 = 0;  // chunk sums: |X| <= 2^60 (loss), 2^52 (K1, K3)
+    unsigned cn = 0, ccl = 0, cz = 0;
 #pragma unroll
     for (int k = 0; k < kPpoTpl; ++k) {
-      const long long i = i0 + k;
-      if (i >= p.n) continue;
-      const long long g = p.tok_begin + i;
-      const double d = dv[k];
-      if (!isfinite(d)) {
-        const unsigned long long b = kBadSentinel - static_cast<unsigned long long>(g);
-        bad_inv = b > bad_inv ? b : bad_inv;
-        p.loss[i] = CUDART_NAN_F;
-        p.grad[i] = 0.f;
-        p.clipped[i] = 0;
-        continue;
-      }
-      const double r = rv[k];
-      const double A = static_cast<double>(adv[k]);
+      const bool tiny = fabs(dv[k]) <= kSmall;
+      const double d = tiny ? ds[k] : dm[k];
+      const double k3 = tiny ? k3s[k] : k3m[k];
+      const double r = tiny ? exp_from_k3_small(ds[k], k3s[k]) : em[k];
+      const double A = static_cast<double>(ad_[k]);
       const bool clipped = (A > 0.0 && r > p.clip_hi) || (A < 0.0 && r < p.clip_lo);
       const double sv = clipped ? __dmul_rn(A > 0.0 ? p.clip_hi : p.clip_lo, A) : __dmul_rn(r, A);
-      const double loss = -__dmul_rn(static_cast<double>(wv[k]), sv);
-      p.loss[i] = __double2float_rn(loss);
-      p.grad[i] = clipped ? 0.f : __double2float_rn(loss);
-      p.clipped[i] = clipped ? 1 : 0;
-      // leave the sequence(s) the lane has walked past
-      while (g >= next_b) {
-        flush_seq(p.seqp, acc);
-        acc.x = 0;
-        acc.t = 0;
-        acc.nsat = 0;
-        acc.sid += 1;
-        next_b = __ldg(p.cu + acc.sid + 1);
+      const double loss = -__dmul_rn(static_cast<double>(wv_[k]), sv);
+      if (!(fabs(loss) <= kPpoFastLoss)) slow |= 1u << k;
+      const float lf = __double2float_rn(loss);
+      l_out[k] = lf;
+      g_out[k] = clipped ? 0.f : lf;
+      cbits |= static_cast<uint32_t>(clipped) << (8 * k);
+      const bool use = wv_[k] != 0.f && !((slow >> k) & 1u);
+      const double lz = use ? loss : 0.0;
+      const double dz = use ? d : 0.0;
+      const double kz = use ? k3 : 0.0;
+      cl += __double2ll_rn(__dmul_rn(lz, kTwo52));
+      ck1 += __double2ll_rn(__dmul_rn(-dz, kTwo52));
+      ck3 += __double2ll_rn(__dmul_rn(kz, kTwo52));
+      cn += use ? 1u : 0u;
+      ccl += (use && clipped) ? 1u : 0u;
+      cz += (use && A == 0.0) ? 1u : 0u;
+      if (use && A != 0.0) atomicAdd(&sh_hist[(A > 0.0 ? 0 : nslot) + hist_slot(p, r, A)], 1);
+    }
+    s_loss += cl;
+    acc.x += cl;
+    acc.t += cn;
+    s_k1 += ck1;
+    s_k3 += ck3;
+    c_contrib += cn;
+    c_clip += ccl;
+    c_zero += cz;
+
+    if (slow) {  // rare: the full contract per token in the slow tokens' lanes
+#pragma unroll
+      for (int k = 0; k < kPpoTpl; ++k) {
+        if (!((slow >> k) & 1u)) continue;
+        const long long i = i0 + k;
+        if (i >= p.n) continue;
+        const long long g = p.tok_begin + i;
+        const double d = dv[k];
+        while (g >= next_b) {  // leave the sequence(s) the lane has walked past
+          flush_seq(p.seqp, acc);
+          acc.x = 0;
+          acc.t = 0;
+          acc.nsat = 0;
+          acc.sid += 1;
+          next_b = __ldg(p.cu + acc.sid + 1);
+        }
+        if (!isfinite(d)) {
+          const unsigned long long b = kBadSentinel - static_cast<unsigned long long>(g);
+          bad_inv = b > bad_inv ? b : bad_inv;
+          l_out[k] = CUDART_NAN_F;
+          g_out[k] = 0.f;
+          cbits &= ~(0xffu << (8 * k));
+          continue;
+        }
+        const double k3 = k3_c(d);
+        const double r = exp_c(d);
+        const double A = static_cast<double>(ad_[k]);
+        const bool clipped = (A > 0.0 && r > p.clip_hi) || (A < 0.0 && r < p.clip_lo);
+        const double sv = clipped ? __dmul_rn(A > 0.0 ? p.clip_hi : p.clip_lo, A) : __dmul_rn(r, A);
+        const double loss = -__dmul_rn(static_cast<double>(wv_[k]), sv);
+        l_out[k] = __double2float_rn(loss);
+        g_out[k] = clipped ? 0.f : l_out[k];
+        cbits = (cbits & ~(0xffu << (8 * k))) | (static_cast<uint32_t>(clipped) << (8 * k));
+        if (wv_[k] == 0.f) continue;
+        bool sat, sat1, sat3;
+        const long long X = fixed_point(loss, sat);
+        const long long X1 = fixed_point(-d, sat1);
+        const long long X3 = fixed_point(k3, sat3);
+        c_contrib += 1;
+        c_clip += clipped ? 1u : 0u;
+        c_sat += sat ? 1u : 0u;
+        s_loss += X;
+        s_k1 += X1;
+        s_k3 += X3;
+        acc.x += X;
+        acc.t += 1;
+        acc.nsat += sat ? 1 : 0;
+        if (A == 0.0) c_zero += 1;
+        else atomicAdd(&sh_hist[(A > 0.0 ? 0 : nslot) + hist_slot(p, r, A)], 1);
       }
-      if (!cb[k]) continue;
-      bool sat, sat1, sat3;
-      const long long X = fixed_point(loss, sat);
-      const long long X1 = fixed_point(-d, sat1);
-      const long long X3 = fixed_point(k3_c(d), sat3);
-      c_contrib += 1;
-      c_clip += clipped ? 1 : 0;
-      c_sat += sat ? 1 : 0;
-      s_loss += X;
-      s_k1 += X1;
-      s_k3 += X3;
-      acc.x += X;
-      acc.t += 1;
-      acc.nsat += sat ? 1 : 0;
-      if (A == 0.0) {
-        c_zero += 1;
-      } else {
-        const double C = __dmul_rn(-__dsub_rn(r, 1.0), A);
-        const double raw = floor(__dmul_rn(__dsub_rn(C, p.hist_lo), p.hist_inv_width));
-        const int slot = raw < 0.0 ? 0 : (raw >= static_cast<double>(p.bins) ? p.bins + 1 : static_cast<int>(raw) + 1);
-        atomicAdd(&sh_hist[(A > 0.0 ? 0 : nslot) + slot], 1);
+    }
+
+    if (full) {
+      __stcs(reinterpret_cast<float4*>(p.loss + i0), make_float4(l_out[0], l_out[1], l_out[2], l_out[3]));
+      __stcs(reinterpret_cast<float4*>(p.grad + i0), make_float4(g_out[0], g_out[1], g_out[2], g_out[3]));
+      __stcs(reinterpret_cast<unsigned int*>(p.clipped + i0), cbits);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kPpoTpl; ++k) {
+        const long long i = i0 + k;
+        if (i < p.n) {
+          p.loss[i] = l_out[k];
+          p.grad[i] = g_out[k];
+          p.clipped[i] = (cbits >> (8 * k)) & 0xffu;
+        }
       }
     }
   }
-
   // the open sequence segments of the warp (ids are non-decreasing in lane order)
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
@@ -158,20 +280,20 @@ __global__ void __launch_bounds__(kPpoThreads, 2) ppo_local_kernel(PpoLocalParam
   if ((lane == 0 || prev_sid != acc.sid) && acc.sid != LLONG_MAX) flush_seq(p.seqp, acc);
 
   // global counters: warp reduce, then integer atomics (exact)
-  c_contrib = warp_sum_i64(c_contrib);
-  c_clip = warp_sum_i64(c_clip);
-  c_zero = warp_sum_i64(c_zero);
-  c_sat = warp_sum_i64(c_sat);
+  const long long n_contrib = warp_sum_i64(c_contrib);
+  const long long n_clip = warp_sum_i64(c_clip);
+  const long long n_zero = warp_sum_i64(c_zero);
+  const long long n_sat = warp_sum_i64(c_sat);
   s_loss = warp_sum_i128(s_loss);
   s_k1 = warp_sum_i128(s_k1);
   s_k3 = warp_sum_i128(s_k3);
   bad_inv = warp_max_u64(bad_inv);
   tim_ppo_partial_header* h = p.hdr;
   if (lane == 0) {
-    if (c_contrib) atomicAdd(reinterpret_cast<unsigned long long*>(&h->n_contrib), static_cast<unsigned long long>(c_contrib));
-    if (c_clip) atomicAdd(reinterpret_cast<unsigned long long*>(&h->n_clipped), static_cast<unsigned long long>(c_clip));
-    if (c_zero) atomicAdd(reinterpret_cast<unsigned long long*>(&h->n_zero_adv), static_cast<unsigned long long>(c_zero));
-    if (c_sat) atomicAdd(reinterpret_cast<unsigned long long*>(&h->n_saturated), static_cast<unsigned long long>(c_sat));
+    if (n_contrib) atomicAdd(reinterpret_cast<unsigned long long*>(&h->n_contrib), static_cast<unsigned long long>(n_contrib));
+    if (n_clip) atomicAdd(reinterpret_cast<unsigned long long*>(&h->n_clipped), static_cast<unsigned long long>(n_clip));
+    if (n_zero) atomicAdd(reinterpret_cast<unsigned long long*>(&h->n_zero_adv), static_cast<unsigned long long>(n_zero));
+    if (n_sat) atomicAdd(reinterpret_cast<unsigned long long*>(&h->n_saturated), static_cast<unsigned long long>(n_sat));
     atomic_add_i128(h->sum_loss, s_loss);
     atomic_add_i128(h->sum_k1, s_k1);
     atomic_add_i128(h->sum_k3, s_k3);
@@ -256,7 +378,7 @@ int ppo_max_hist_bins() { return kMaxHistBins; }
 cudaError_t launch_ppo_local(const PpoLocalParams& p, int num_sms, cudaStream_t stream) {
   const long long chunks = (p.n + kPpoWarpTok - 1) / kPpoWarpTok;
   long long blocks = (chunks + kPpoThreads / 32 - 1) / (kPpoThreads / 32);
-  const long long cap = static_cast<long long>(num_sms) * 2;
+  const long long cap = static_cast<long long>(num_sms) * kPpoMinB;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   const size_t smem = sizeof(int) * 2 * (p.bins + 2);

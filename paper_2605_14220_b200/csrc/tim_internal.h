@@ -173,6 +173,7 @@ struct PpoLocalParams {
   int64_t* hist;         // [2][bins + 2] inside the partial block
   tim_seq_partial* seqp;
   tim_device_status* dstatus;
+  int vec;               // every per-token array allows 16-B (4-B for u8) vector accesses
 };
 struct PpoFinishParams {
   const uint8_t* gathered;
