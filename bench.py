@@ -99,13 +99,14 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def _traffic():
-    """dram bytes per launch of the logprob kernel from the committed ncu --set full summary."""
+def _traffic(config: str):
+    """dram bytes per launch of the logprob kernel on this config, from the committed ncu --set
+    full summary (None when no capture of this config is committed)."""
     p = os.path.join(ROOT, "profiles", "ncu_logprob_summary.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("dram_bytes_per_launch_c1")
+        return d.get(f"dram_bytes_per_launch_{config}")
     except Exception:
         return None
 
@@ -236,6 +237,30 @@ def run_ours(args):
                        "logp_bitwise_equal_to_logprob": same,
                        "kernel": "tim_sample (tcgen05 GEMM + online LSE + Philox Gumbel-max epilogue)"}
 
+    # NEXT-3 head backward on one token block of the batch (dL/dlogp = 1, dL/dH = 0.01)
+    bwd_info = None
+    if args.backward_bench:
+        nb = min(N, 14080)
+        gl = torch.ones(nb, device=dev)
+        ge = torch.full((nb,), 0.01, device=dev)
+        for _ in range(2):
+            dh, dw = tim.head_backward(H[:nb], W, ids[:nb], gl, ge)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            dh, dw = tim.head_backward(H[:nb], W, ids[:nb], gl, ge)
+        e1.record()
+        torch.cuda.synchronize()
+        bms = e0.elapsed_time(e1) / 3
+        bwd_info = {"tokens": nb, "ms": bms, "tokens_per_s": nb / (bms / 1e3),
+                    "tflops_effective": 4 * 2.0 * cfg.vocab * cfg.hidden * nb / (bms / 1e3) / 1e12,
+                    "note": "4 passes of 2 V d flop per token: forward, gradient epilogue (logits recomputed), "
+                            "dH = G W and dW = G^T H (cuBLAS)",
+                    "kernel": "tim_head_backward"}
+        del dh, dw
+        torch.cuda.empty_cache()
+
     # end to end through the public API from pinned host buffers
     e2e = None
     Hh = H.cpu().pin_memory()
@@ -302,7 +327,7 @@ def run_ours(args):
         "gpu_launches": KERNELS_PER_STEP * args.steps,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "frac_of_burst": achieved / float(peaks["bf16_tflops"]),
-                     "peak_source": peak_src + " bf16_tflops_sustained", "traffic": _traffic(),
+                     "peak_source": peak_src + " bf16_tflops_sustained", "traffic": _traffic(cfg.name),
                      "kernel": "tim_logprob (tcgen05 GEMM + fused epilogue + slice merge)",
                      "kernel_ms": lp_ms, "algorithmic_flop_per_token": 2 * cfg.vocab * cfg.hidden},
         "clocks": clk,
@@ -312,6 +337,8 @@ def run_ours(args):
     }
     if sample_info is not None:
         out["sample_twin"] = sample_info
+    if bwd_info is not None:
+        out["head_backward"] = bwd_info
     if args.correction_tokens > 0:
         out["correction_roofline"] = correction_roofline(tim, dev, args.correction_tokens, peaks, peak_src)
         out["ppo_roofline"] = ppo_roofline(tim, dev, args.correction_tokens, peaks, peak_src)
@@ -497,6 +524,8 @@ def main():
     ap.add_argument("--max-pairs", type=int, default=0, help="cap the persistent grid (experiments)")
     ap.add_argument("--n-seq", type=int, default=0, help="override the number of sequences (experiments)")
     ap.add_argument("--cluster-pairs", type=int, default=0, help="1 or 2 CTA pairs per cluster (experiments)")
+    ap.add_argument("--no-backward-bench", dest="backward_bench", action="store_false",
+                    help="skip the NEXT-3 head-backward timing")
     ap.add_argument("--no-sample-bench", dest="sample_bench", action="store_false",
                     help="skip the rollout-side twin (tim_sample) measurement")
     args = ap.parse_args()
