@@ -457,10 +457,24 @@ def cpu_baseline(cfg, W, Hh, ids, lp_gpu, lp_roll, mask, seconds):
     oc.correct(lp_gpu[:n_corr].cpu().numpy(), lp_roll[:n_corr].cpu().numpy(), cu, ocfg, mask[:n_corr].cpu().numpy())
     t_corr = time.perf_counter() - t
     per_tok = t_lp / done + t_corr / n_corr
+    # the same oracle pinned to one BLAS thread, on a smaller sample
+    one = None
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+        blas = ",".join(sorted({f"{d.get('internal_api')}({d.get('num_threads')})" for d in threadpool_info()
+                                if d.get("user_api") == "blas"}))
+        with threadpool_limits(limits=1, user_api="blas"):
+            r = rows[:32]
+            t = time.perf_counter()
+            logprob_entropy(Hh[r], Wc, ids.cpu()[r], row_chunk=32)
+            one = 32 / (time.perf_counter() - t)
+    except Exception:
+        blas = "unknown"
     return ({"value": 1.0 / per_tok, "unit": "tokens/s", "cores": _blas_threads(), "kind": "oracle",
              "sample": f"fp64 numpy oracle: logprob+entropy on {done} random rows of the {cfg.name} batch "
                        f"({t_lp:.1f} s) + correction (tis-srs-k3) on {n_corr} tokens ({t_corr:.1f} s); "
-                       f"host {os.cpu_count()} logical cpus"}, dmax)
+                       f"host {os.cpu_count()} logical cpus; BLAS {blas}",
+             "logprob_tokens_per_s_1_thread": one}, dmax)
 
 
 def run_reference(args):

@@ -147,6 +147,9 @@ tim_status tim_sample(const void* hidden_bf16, int64_t ld_hidden,
  *                       Sequences may straddle ranks.
  *   resp_mask_or_null   [n_tok_local] u8 (1 = response token); NULL = all response (U11).
  * Only response tokens enter K sums, T_s and statistics; non-response tokens get coeff 0.
+ * Alignment: fp32 arrays 4-B aligned (TIM_ERR_ALIGN otherwise).  When every per-token array
+ * is 16-B aligned (u8 arrays 4-B) the kernels use 16-B vector accesses; otherwise (e.g. a
+ * shard cut at an arbitrary token) the same results come from the scalar path, slower.
  * -------------------------------------------------------------------------- */
 typedef enum { TIM_SEQ_NONE = 0, TIM_SEQ_K1 = 1, TIM_SEQ_K3 = 3 } tim_seq_rs;
 typedef enum { TIM_AGG_SUM = 0, TIM_AGG_MEAN = 1 } tim_agg;

@@ -282,7 +282,7 @@ tim_status check_common(const float* num, const float* den, const int64_t* cu, i
   if (n_local > 0 && (!num || !den)) return TIM_ERR_NULL;
   if (n_seq < 0 || n_seq >= (int64_t(1) << 40) || n_local < 0 || tok_begin < 0) return TIM_ERR_SHAPE;
   if (n_local > 0 && n_seq == 0) return TIM_ERR_SHAPE;
-  if (!aligned(num, 16) || !aligned(den, 16) || (resp && !aligned(resp, 8))) return TIM_ERR_ALIGN;
+  if (!aligned(num, 4) || !aligned(den, 4)) return TIM_ERR_ALIGN;  // 16-B aligned arrays take the vector path
   return TIM_OK;
 }
 
@@ -503,6 +503,8 @@ tim_status tim_correct_local(const float* num, const float* den, const int64_t* 
   p.seqp = reinterpret_cast<tim_seq_partial*>(static_cast<uint8_t*>(partial_out) + sizeof(tim_partial_header));
   p.cfg = dev_cfg(cfg);
   p.dstatus = dstatus;
+  p.vec = aligned(num, 16) && aligned(den, 16) && aligned(resp, 4) && aligned(tis_w, 16) && aligned(coeff, 16) &&
+          aligned(tok_keep, 4);
   return launch_correct_local(p, dev->num_sms, s) == cudaSuccess ? TIM_OK : TIM_ERR_CUDA;
 }
 
@@ -918,7 +920,7 @@ tim_status tim_ppo_local(const float* cur, const float* old, const float* adv, c
   p.seqp = reinterpret_cast<tim_seq_partial*>(blk + sizeof(tim_ppo_partial_header) +
                                               16u * static_cast<size_t>(cfg->hist_bins + 2));
   p.dstatus = dstatus;
-  p.vec = aligned(adv, 16) && aligned(coeff, 16) && aligned(loss, 16) && aligned(grad, 16) && aligned(clipped, 4) &&
+  p.vec = aligned(cur, 16) && aligned(old, 16) && aligned(adv, 16) && aligned(coeff, 16) && aligned(loss, 16) && aligned(grad, 16) && aligned(clipped, 4) &&
           aligned(resp, 4);
   return launch_ppo_local(p, dev->num_sms, s) == cudaSuccess ? TIM_OK : TIM_ERR_CUDA;
 }

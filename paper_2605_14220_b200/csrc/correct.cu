@@ -11,8 +11,8 @@
 // into exact 2^-52 fixed point and all sums are int128 integer sums -- exact, so independent of
 // the reduction order, of atomics order, of sharding and of the GPU count.
 //
-// Layout: structure-of-arrays fp32 / u8 token vectors, one warp owns 256 consecutive tokens
-// (8 per lane, 32-B vector loads), so every load and store is fully coalesced.
+// Layout: structure-of-arrays fp32 / u8 token vectors, one warp owns 128 consecutive tokens
+// (4 per lane, 16-B vector loads and stores), so every load and store is fully coalesced.
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
@@ -47,7 +47,7 @@ struct Chunk {
 
 __device__ __forceinline__ Chunk load_chunk(const LocalParams& p, long long i0) {
   Chunk c;
-  if (i0 + kTpl <= p.n) {
+  if (p.vec && i0 + kTpl <= p.n) {
     c.num = __ldcs(reinterpret_cast<const float4*>(p.num + i0));
     c.den = __ldcs(reinterpret_cast<const float4*>(p.den + i0));
     c.resp = p.resp ? __ldcs(reinterpret_cast<const unsigned int*>(p.resp + i0)) : 0x01010101u;
@@ -118,7 +118,8 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
     const float den[4] = {cur.den.x, cur.den.y, cur.den.z, cur.den.w};
 
     double dv[kTpl], ds[kTpl], k3s[kTpl];
-    unsigned slow = i0 + kTpl <= p.n ? 0u : 0xFu;
+    const bool full = p.vec && i0 + kTpl <= p.n;
+    unsigned slow = full ? 0u : 0xFu;
     if (kSeq && p.tok_begin + i0 + (kTpl - 1) >= next_b) slow = 0xFu;
 #pragma unroll
     for (int k = 0; k < kTpl; ++k) {
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
     }
 
     if (kOut) {
-      if (i0 + kTpl <= p.n) {
+      if (full) {
         __stcs(reinterpret_cast<float4*>(p.tis_w + i0), make_float4(w_out[0], w_out[1], w_out[2], w_out[3]));
         __stcs(reinterpret_cast<float4*>(p.coeff + i0), make_float4(c_out[0], c_out[1], c_out[2], c_out[3]));
         __stcs(reinterpret_cast<unsigned int*>(p.tok_keep + i0), kbits);

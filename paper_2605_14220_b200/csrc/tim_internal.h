@@ -134,6 +134,7 @@ struct LocalParams {
   tim_seq_partial* seqp;
   CorrectDevCfg cfg;
   tim_device_status* dstatus;
+  int vec;            // every per-token array allows 16-B (4-B for u8) vector accesses
 };
 struct FinishParams {
   const uint8_t* gathered;  // [nranks][block_bytes]

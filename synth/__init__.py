@@ -136,6 +136,17 @@ def perturb_bf16(lp: torch.Tensor) -> torch.Tensor:
     return lp.to(torch.bfloat16).to(torch.float32)
 
 
+def perturb_hidden_ulp(H: torch.Tensor, p: float, seed: int) -> torch.Tensor:
+    """P2: move random bf16 elements of H by one ulp (+-1 on the bit pattern) with probability
+    p; the trainer side then re-scores the perturbed rows (an upstream-kernel
+    style mismatch)."""
+    g = _gen(seed * 7 + 7, H.device)
+    bits = H.contiguous().view(torch.int16)
+    flip = torch.rand(bits.shape, generator=g, device=H.device) < p
+    step = torch.where(torch.rand(bits.shape, generator=g, device=H.device) < 0.5, -1, 1).to(torch.int16)
+    return torch.where(flip, bits + step, bits).view(torch.bfloat16)
+
+
 def perturb_laplace_mix(lp: torch.Tensor, seed: int, p_zero: float = 0.5, small: float = 2e-3,
                         p_big: float = 0.001, big: float = 0.25) -> torch.Tensor:
     """P3: delta = 0 w.p. p_zero, else Laplace(0, small) w.p. (1-p_zero-p_big), else
