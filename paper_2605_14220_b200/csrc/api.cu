@@ -508,9 +508,11 @@ tim_status tim_correct_local(const float* num, const float* den, const int64_t* 
   return launch_correct_local(p, dev->num_sms, s) == cudaSuccess ? TIM_OK : TIM_ERR_CUDA;
 }
 
-tim_status tim_correct_finish(const void* gathered, int32_t nranks, const int64_t* cu, int64_t n_seq,
-                              int64_t tok_begin, int64_t n_local, const tim_correct_cfg* cfg, float* coeff,
-                              uint8_t* seq_keep, double* seq_score, tim_stats* stats, void* stream) {
+// scratch: 2 zeroed words for a multi-block finish (or null: one block)
+static tim_status correct_finish_impl(const void* gathered, int32_t nranks, const int64_t* cu, int64_t n_seq,
+                                      int64_t tok_begin, int64_t n_local, const tim_correct_cfg* cfg, float* coeff,
+                                      uint8_t* seq_keep, double* seq_score, tim_stats* stats,
+                                      unsigned long long* scratch, void* stream) {
   if (!gathered || !cu) return TIM_ERR_NULL;
   if (nranks < 1 || n_seq < 0 || n_local < 0 || tok_begin < 0) return TIM_ERR_SHAPE;
   tim_status st = check_cfg(cfg);
@@ -529,7 +531,8 @@ tim_status tim_correct_finish(const void* gathered, int32_t nranks, const int64_
   f.seq_keep = seq_keep;
   f.seq_score = seq_score;
   f.stats = stats;
-  if (launch_correct_finish(f, s) != cudaSuccess) return TIM_ERR_CUDA;
+  f.scratch = scratch;
+  if (launch_correct_finish(f, dev->num_sms, s) != cudaSuccess) return TIM_ERR_CUDA;
   if (cfg->seq_rs != TIM_SEQ_NONE && n_local > 0 && n_seq > 0) {
     if (!seq_keep) return TIM_ERR_NULL;
     ZeroParams z{};
@@ -542,6 +545,13 @@ tim_status tim_correct_finish(const void* gathered, int32_t nranks, const int64_
     if (launch_correct_zero(z, s) != cudaSuccess) return TIM_ERR_CUDA;
   }
   return TIM_OK;
+}
+
+tim_status tim_correct_finish(const void* gathered, int32_t nranks, const int64_t* cu, int64_t n_seq,
+                              int64_t tok_begin, int64_t n_local, const tim_correct_cfg* cfg, float* coeff,
+                              uint8_t* seq_keep, double* seq_score, tim_stats* stats, void* stream) {
+  return correct_finish_impl(gathered, nranks, cu, n_seq, tok_begin, n_local, cfg, coeff, seq_keep, seq_score, stats,
+                             nullptr, stream);
 }
 
 static tim_status correct_impl(const float* num, const float* den, const int64_t* cu, int64_t n_seq,
@@ -573,8 +583,12 @@ static tim_status correct_impl(const float* num, const float* den, const int64_t
       return TIM_ERR_NCCL;
     gathered = g;
   }
-  return tim_correct_finish(gathered, nranks, cu, n_seq, tok_begin, n_local, cfg, coeff, seq_keep, seq_score, stats,
-                            stream);
+  // the local block's header reserved[2..3] (zeroed with the block; pass 1 uses [0..1]) serve as
+  // the finish pass's {ticket, rejections}
+  unsigned long long* scratch =
+      reinterpret_cast<unsigned long long*>(&reinterpret_cast<tim_partial_header*>(local)->reserved[2]);
+  return correct_finish_impl(gathered, nranks, cu, n_seq, tok_begin, n_local, cfg, coeff, seq_keep, seq_score, stats,
+                             scratch, stream);
 }
 
 tim_status tim_mismatch_stats(const float* num, const float* den, const int64_t* cu, int64_t n_seq,

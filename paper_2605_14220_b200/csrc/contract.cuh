@@ -182,4 +182,13 @@ __device__ __forceinline__ __int128 seq_threshold(double tau, long long T) {
 }
 
 
+// Sequence keep (C.3 step 9): T_s = 0 keeps, a saturated token rejects, else the exact int128
+// compare X_s <= floor(tau 2^52) (SUM) or floor(tau 2^52 T_s) (MEAN).
+__device__ __forceinline__ bool seq_keep_decision(double tau_seq, int seq_agg, __int128 X, long long T,
+                                                  long long nsat) {
+  if (T == 0) return true;
+  if (nsat > 0) return false;
+  return X <= seq_threshold(tau_seq, seq_agg == TIM_AGG_MEAN ? T : 1);
+}
+
 }  // namespace tim

@@ -19,26 +19,34 @@
 #include <cstdint>
 
 #include "contract.cuh"
+#include "ptx.cuh"
 #include "tim_internal.h"
 
 namespace tim {
 
 #ifndef TIM_CORR_MINB
-#define TIM_CORR_MINB 3
+#define TIM_CORR_MINB 5
 #endif
 constexpr int kTpl = 4;                 // tokens per lane (one float4 of num / den, one u32 of resp)
 constexpr int kWarpTok = 32 * kTpl;     // tokens per warp chunk
-constexpr int kLocalThreads = 256;
-constexpr int kFlushChunks = 4096;      // fast-path int64 sums are folded into int128 this often
+constexpr int kLocalThreads = 128;
+constexpr int kLocalWarps = kLocalThreads / 32;
+constexpr int kStages = 4;              // per-warp TMA ring: chunks of num / den in flight
+constexpr int kFoldChunks = 16;        // the exact fp64 chunk sums are folded into int128 this often
 
-// Per-thread rarely-touched state (int128 sums of the slow path, data errors), in shared memory
-// so the hot loop keeps its registers for the loads in flight and the Horner chains.
-struct SlowAcc {
+// Per-thread state that the fast path does not touch every chunk, in shared memory so the hot
+// loop keeps its registers for the loads in flight and the Horner chains: the int128 sums, the
+// sequence walk, and the counters of the (out-of-line) mixed-chunk path.
+struct LaneState {
   __int128 s_abs, s_k1, s_k3, seq_x;
   unsigned long long bad_inv;
   long long c_sat, seq_nsat;
-  long long pad;
+  long long sid, next_b, seq_t;
+  double mx;
+  unsigned c_resp, c_trunc, c_rej, pad;
+  long long pad2;
 };
+static_assert(sizeof(LaneState) % 16 == 0, "LaneState alignment");
 
 struct Chunk {
   float4 num, den;
@@ -68,67 +76,72 @@ __device__ __forceinline__ Chunk load_chunk(const LocalParams& p, long long i0) 
   return c;
 }
 
-// Pass 1 (a5).  Every warp owns a contiguous run of 128-token chunks (4 tokens per lane, the
-// next chunk's loads in flight while the current one computes).  Fast path, all lanes in
-// lockstep: tokens with |delta| <= 2^-6 (finite by construction) use the short contract
-// polynomials; their K values cannot saturate (|K| <= 2^-6), so they accumulate in int64
-// (|X| <= 2^46, folded into int128 every kFlushChunks chunks).  Slow path, per lane and rare:
-// larger or non-finite delta, a partial chunk, or a sequence boundary inside the lane's four
-// tokens -- the full per-token contract with int128 sums and the sequence walk.
-template <bool kOut, bool kSeq, bool kTis, bool kTokRs>
-__global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_kernel(LocalParams p) {
-  __shared__ SlowAcc sh_slow[kLocalThreads];
-  const int lane = threadIdx.x & 31;
-  const long long warp_g = (static_cast<long long>(blockIdx.x) * kLocalThreads + threadIdx.x) >> 5;
-  const long long nwarps = (static_cast<long long>(gridDim.x) * kLocalThreads) >> 5;
-  const long long n_chunks = (p.n + kWarpTok - 1) / kWarpTok;
-  const CorrectDevCfg cfg = p.cfg;
-  SlowAcc& sa = sh_slow[threadIdx.x];
-  sa.s_abs = 0;
-  sa.s_k1 = 0;
-  sa.s_k3 = 0;
-  sa.seq_x = 0;
-  sa.bad_inv = 0;
-  sa.c_sat = 0;
-  sa.seq_nsat = 0;
+__device__ __forceinline__ Chunk load_vec(const LocalParams& p, long long i0) {
+  Chunk c;
+  c.num = __ldcs(reinterpret_cast<const float4*>(p.num + i0));
+  c.den = __ldcs(reinterpret_cast<const float4*>(p.den + i0));
+  c.resp = p.resp ? __ldcs(reinterpret_cast<const unsigned int*>(p.resp + i0)) : 0x01010101u;
+  return c;
+}
 
-  unsigned c_resp = 0, c_trunc = 0, c_rej = 0;
-  long long f_abs = 0, f_k1 = 0, f_k3 = 0, f_seq = 0;  // fast-path exact sums
-  double mx = 0.0;                                     // max |delta| (finite response tokens)
-  long long seq_t = 0;
-
-  const long long cpw = (n_chunks + nwarps - 1) / nwarps;
-  const long long c_begin = warp_g * cpw;
-  const long long c_end = c_begin + cpw < n_chunks ? c_begin + cpw : n_chunks;
-  long long sid = LLONG_MAX, next_b = LLONG_MAX;
-  if (kSeq && c_begin < c_end && c_begin * kWarpTok + lane * kTpl < p.n) {
-    sid = seq_of(p.cu, p.n_seq, p.tok_begin + c_begin * kWarpTok + lane * kTpl);
-    next_b = __ldg(p.cu + sid + 1);
-  }
-  const bool seq_k1 = cfg.seq_rs == TIM_SEQ_K1;
-  const float cap_f = __double2float_rn(cfg.tis_cap);
-
-  Chunk nxt;
-  if (c_begin < c_end) nxt = load_chunk(p, c_begin * kWarpTok + lane * kTpl);
-  for (long long ch = c_begin; ch < c_end; ++ch) {
-    const long long i0 = ch * kWarpTok + lane * kTpl;
-    const Chunk cur = nxt;
-    if (ch + 1 < c_end) nxt = load_chunk(p, i0 + kWarpTok);
-    const float num[4] = {cur.num.x, cur.num.y, cur.num.z, cur.num.w};
-    const float den[4] = {cur.den.x, cur.den.y, cur.den.z, cur.den.w};
-
-    double dv[kTpl], ds[kTpl], k3s[kTpl];
-    const bool full = p.vec && i0 + kTpl <= p.n;
-    unsigned slow = full ? 0u : 0xFu;
-    if (kSeq && p.tok_begin + i0 + (kTpl - 1) >= next_b) slow = 0xFu;
+__device__ __forceinline__ void store_chunk(const LocalParams& p, long long i0, bool full, const float* w_out,
+                                            const float* c_out, uint32_t kbits) {
+  if (full) {
+    __stcs(reinterpret_cast<float4*>(p.tis_w + i0), make_float4(w_out[0], w_out[1], w_out[2], w_out[3]));
+    __stcs(reinterpret_cast<float4*>(p.coeff + i0), make_float4(c_out[0], c_out[1], c_out[2], c_out[3]));
+    __stcs(reinterpret_cast<unsigned int*>(p.tok_keep + i0), kbits);
+  } else {
 #pragma unroll
     for (int k = 0; k < kTpl; ++k) {
-      dv[k] = __dsub_rn(static_cast<double>(num[k]), static_cast<double>(den[k]));
-      const bool sm = fabs(dv[k]) <= kSmall;  // false for NaN / inf
-      if (!sm) slow |= 1u << k;
-      ds[k] = sm ? dv[k] : 0.0;
+      const long long i = i0 + k;
+      if (i < p.n) {
+        p.tis_w[i] = w_out[k];
+        p.coeff[i] = c_out[k];
+        p.tok_keep[i] = (kbits >> (8 * k)) & 0xffu;
+      }
     }
-    // short K3 series of the four tokens in lockstep (independent Horner chains)
+  }
+}
+
+// K3 and e^delta of a token outside the short-polynomial range (rare; out of line so the
+// chunk loop keeps its registers and stays in the instruction cache).
+__device__ __noinline__ double2 k3_exp_full(double d) { return make_double2(k3_c(d), exp_c(d)); }
+
+// Fast-path register state of a lane: exact fp64 sums of quantised values (each an integer with
+// |X| <= 2^46, so 16 chunks of four sum exactly, < 2^52), max |delta| and counters.
+struct FastAcc {
+  double k1, k3, ab, seq, mx;
+  unsigned resp, trunc, rej, seq_t;
+};
+
+// One chunk (four tokens per lane), the short contract polynomials for every token with
+// |delta| <= 2^-6 in lock-step.  kMasked = false: the warp-uniform common case -- every token
+// small, no sequence boundary inside any lane's tokens, the response mask all-1 (sum_on) or
+// all-0 over the chunk; no per-token selects.  kMasked = true: per-token masks, and the slow
+// tokens (larger or non-finite delta, partial chunk, sequence boundary) then take the full
+// contract per lane with int128 sums and the sequence walk in the lane's shared-memory state.
+template <bool kMasked, bool kOut, int kSeqK, bool kTis, bool kTokRs>
+__device__ __forceinline__ void chunk_body(const LocalParams& p, LaneState& st, FastAcc& fa, const float4 numv,
+                                           const float4 denv, const uint32_t resp_bits, const long long i0,
+                                           const bool full, const bool lane_whole, const bool sum_on,
+                                           const double (&dv)[kTpl]) {
+  constexpr bool kSeq = kSeqK != TIM_SEQ_NONE;
+  constexpr bool seq_k1 = kSeqK == TIM_SEQ_K1;
+  const CorrectDevCfg& cfg = p.cfg;
+  const float cap_f = __double2float_rn(cfg.tis_cap);
+  unsigned slow = 0;
+  double ds[kTpl], k3s[kTpl];
+#pragma unroll
+  for (int k = 0; k < kTpl; ++k) {
+    if (kMasked) {
+      const bool sm = fabs(dv[k]) <= kSmall;  // false for NaN / inf
+      if (!sm || !lane_whole) slow |= 1u << k;
+      ds[k] = sm ? dv[k] : 0.0;  // slow small tokens reuse their k3s
+    } else {
+      ds[k] = dv[k];
+    }
+  }
+  if (kMasked || kTis || sum_on) {  // short K3 series, four independent Horner chains
     double q[kTpl];
 #pragma unroll
     for (int k = 0; k < kTpl; ++k) q[k] = kInvFact[9];
@@ -138,159 +151,286 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
       for (int k = 0; k < kTpl; ++k) q[k] = __dadd_rn(__dmul_rn(q[k], ds[k]), kInvFact[n]);
 #pragma unroll
     for (int k = 0; k < kTpl; ++k) k3s[k] = __dmul_rn(__dmul_rn(ds[k], ds[k]), q[k]);
-
-    float w_out[kTpl], c_out[kTpl];
-    uint32_t kbits = 0;
-    // this chunk's exact sums in fp64: every X is an integer with |X| <= 2^46, so the sums of
-    // four are exact doubles; one conversion per sum per chunk
-    double ck1 = 0.0, ck3 = 0.0, cabs = 0.0, cseq = 0.0, cmx = 0.0;
-    unsigned cn = 0, ctr = 0, crj = 0, cst = 0;
+  }
+  float w_out[kTpl], c_out[kTpl];
+  uint32_t kbits = 0;
+  double cmx = 0.0;
+  unsigned cn = 0, ctr = 0, crj = 0, cst = 0;
 #pragma unroll
-    for (int k = 0; k < kTpl; ++k) {
-      const double d = ds[k];
-      const bool resp = (cur.resp >> (8 * k)) & 0xffu;
-      const bool use = resp && !((slow >> k) & 1u);
-      bool trunc = false;
-      float w = 1.f;
-      if (kTis) {  // (float) min(e, cap) == min((float) e, (float) cap): rounding is monotonic
-        trunc = d > cfg.log_tis_cap;
-        w = trunc ? cap_f : fminf(__double2float_rn(exp_from_k3_small(d, k3s[k])), cap_f);
-      }
-      const bool keep = kTokRs ? (cfg.log_lo <= d && d <= cfg.log_hi) : true;
-      w_out[k] = w;
-      c_out[k] = (resp && keep) ? w : 0.f;
-      kbits |= static_cast<uint32_t>(keep) << (8 * k);
-      const double dz = use ? d : 0.0;  // unused tokens contribute exactly 0 to every sum
-      const double kz = use ? k3s[k] : 0.0;
+  for (int k = 0; k < kTpl; ++k) {
+    const double d = ds[k];
+    const bool resp = kMasked ? ((resp_bits >> (8 * k)) & 0xffu) != 0u : sum_on;
+    const bool use = kMasked ? (resp && !((slow >> k) & 1u)) : sum_on;
+    bool trunc = false;
+    float w = 1.f;
+    if (kTis) {  // (float) min(e, cap) == min((float) e, (float) cap): rounding is monotonic
+      trunc = d > cfg.log_tis_cap;
+      w = trunc ? cap_f : fminf(__double2float_rn(exp_from_k3_small(d, k3s[k])), cap_f);
+    }
+    const bool keep = kTokRs ? (cfg.log_lo <= d && d <= cfg.log_hi) : true;
+    w_out[k] = w;
+    c_out[k] = (resp && keep) ? w : 0.f;
+    kbits |= static_cast<uint32_t>(keep) << (8 * k);
+    if (kMasked || sum_on) {
+      const double dz = kMasked ? (use ? d : 0.0) : d;  // unused tokens add exactly 0
+      const double kz = kMasked ? (use ? k3s[k] : 0.0) : k3s[k];
       const double x1 = rint(__dmul_rn(-dz, kTwo52));  // exact scaling, then round to integer
       const double x3 = rint(__dmul_rn(kz, kTwo52));
-      ck1 = __dadd_rn(ck1, x1);
-      ck3 = __dadd_rn(ck3, x3);
-      cabs = __dadd_rn(cabs, fabs(x1));
-      const double ad = fabs(dz);
-      cmx = ad > cmx ? ad : cmx;
-      cn += use ? 1u : 0u;
+      fa.k1 = __dadd_rn(fa.k1, x1);
+      fa.k3 = __dadd_rn(fa.k3, x3);
+      fa.ab = __dadd_rn(fa.ab, fabs(x1));
+      cmx = fabs(dz) > cmx ? fabs(dz) : cmx;
+      if (kMasked) cn += use ? 1u : 0u;
       if (kTis) ctr += (use && trunc) ? 1u : 0u;
       if (kTokRs) crj += (use && !keep) ? 1u : 0u;
       if (kSeq) {
-        if (kTokRs) cseq = __dadd_rn(cseq, keep ? (seq_k1 ? x1 : x3) : 0.0);
-        cst += (use && keep) ? 1u : 0u;
-      }
-    }
-    const long long ik1 = __double2ll_rn(ck1), ik3 = __double2ll_rn(ck3);
-    f_k1 += ik1;
-    f_k3 += ik3;
-    f_abs += __double2ll_rn(cabs);
-    mx = cmx > mx ? cmx : mx;
-    c_resp += cn;
-    c_trunc += ctr;
-    c_rej += crj;
-    if (kSeq) {
-      f_seq += kTokRs ? __double2ll_rn(cseq) : (seq_k1 ? ik1 : ik3);
-      seq_t += cst;
-    }
-
-    if (slow) {  // rare: the full contract per token, in the slow tokens' lanes only
-#pragma unroll
-      for (int k = 0; k < kTpl; ++k) {
-        if (!((slow >> k) & 1u)) continue;
-        const long long i = i0 + k;
-        if (i >= p.n) continue;
-        const long long g = p.tok_begin + i;
-        const double d = dv[k];
-        if (kSeq) {
-          while (g >= next_b) {  // crossed into a later sequence (skips empty ones)
-            SeqAcc a;
-            a.sid = sid;
-            a.x = sa.seq_x + static_cast<__int128>(f_seq);
-            a.t = seq_t;
-            a.nsat = sa.seq_nsat;
-            flush_seq(p.seqp, a);
-            sa.seq_x = 0;
-            sa.seq_nsat = 0;
-            f_seq = 0;
-            seq_t = 0;
-            sid += 1;
-            next_b = __ldg(p.cu + sid + 1);
-          }
-        }
-        if (!isfinite(d)) {  // C.3.2 data error: excluded from every sum, outputs NaN / 0
-          const unsigned long long b = kBadSentinel - static_cast<unsigned long long>(g);
-          sa.bad_inv = b > sa.bad_inv ? b : sa.bad_inv;
-          w_out[k] = CUDART_NAN_F;
-          c_out[k] = 0.f;
-          kbits &= ~(0xffu << (8 * k));
-          continue;
-        }
-        const bool resp = (cur.resp >> (8 * k)) & 0xffu;
-        const bool sm = fabs(d) <= kSmall;
-        const double k3 = sm ? k3s[k] : k3_c(d);
-        const bool trunc = kTis && d > cfg.log_tis_cap;
-        if (kTis) {
-          const double e = sm ? exp_from_k3_small(d, k3) : exp_c(d);
-          w_out[k] = __double2float_rn(trunc ? cfg.tis_cap : fmin(e, cfg.tis_cap));
-        }
-        const bool keep = kTokRs ? (cfg.log_lo <= d && d <= cfg.log_hi) : true;
-        c_out[k] = (resp && keep) ? w_out[k] : 0.f;
-        kbits = (kbits & ~(0xffu << (8 * k))) | (static_cast<uint32_t>(keep) << (8 * k));
-        if (!resp) continue;
-        bool sat1, sat3;
-        const long long x1 = fixed_point(-d, sat1);
-        const long long x3 = fixed_point(k3, sat3);
-        c_resp += 1;
-        c_trunc += trunc ? 1u : 0u;
-        c_rej += keep ? 0u : 1u;
-        sa.s_abs += x1 < 0 ? -x1 : x1;  // rint is odd-symmetric: X(|delta|) = |X(-delta)|
-        sa.s_k1 += x1;
-        sa.s_k3 += x3;
-        mx = fmax(mx, fabs(d));
-        if (kSeq && keep) {
-          const bool satq = seq_k1 ? sat1 : sat3;
-          sa.seq_x += seq_k1 ? x1 : x3;
-          seq_t += 1;
-          sa.seq_nsat += satq ? 1 : 0;
-          sa.c_sat += satq ? 1 : 0;
+        const double xq = seq_k1 ? x1 : x3;
+        if (kTokRs) {
+          fa.seq = __dadd_rn(fa.seq, keep ? xq : 0.0);
+          cst += (use && keep) ? 1u : 0u;
+        } else {
+          fa.seq = __dadd_rn(fa.seq, xq);
+          if (kMasked) cst += use ? 1u : 0u;
         }
       }
-    }
-
-    if (kOut) {
-      if (full) {
-        __stcs(reinterpret_cast<float4*>(p.tis_w + i0), make_float4(w_out[0], w_out[1], w_out[2], w_out[3]));
-        __stcs(reinterpret_cast<float4*>(p.coeff + i0), make_float4(c_out[0], c_out[1], c_out[2], c_out[3]));
-        __stcs(reinterpret_cast<unsigned int*>(p.tok_keep + i0), kbits);
-      } else {
-#pragma unroll
-        for (int k = 0; k < kTpl; ++k) {
-          const long long i = i0 + k;
-          if (i < p.n) {
-            p.tis_w[i] = w_out[k];
-            p.coeff[i] = c_out[k];
-            p.tok_keep[i] = (kbits >> (8 * k)) & 0xffu;
-          }
-        }
-      }
-    }
-    if (((ch - c_begin) & (kFlushChunks - 1)) == kFlushChunks - 1) {
-      sa.s_abs += f_abs;
-      sa.s_k1 += f_k1;
-      sa.s_k3 += f_k3;
-      sa.seq_x += f_seq;
-      f_abs = f_k1 = f_k3 = f_seq = 0;
     }
   }
+  if (kMasked || sum_on) {
+    fa.mx = cmx > fa.mx ? cmx : fa.mx;
+    fa.resp += kMasked ? cn : kTpl;
+    fa.trunc += ctr;
+    fa.rej += crj;
+    if (kSeq) fa.seq_t += (kMasked || kTokRs) ? cst : kTpl;
+  }
 
-  __int128 s_abs = sa.s_abs + f_abs, s_k1 = sa.s_k1 + f_k1, s_k3 = sa.s_k3 + f_k3;
-  unsigned long long maxbits = static_cast<unsigned long long>(__double_as_longlong(mx));
-  unsigned long long bad_inv = sa.bad_inv;
-  long long c_sat = sa.c_sat;
+  if (kMasked && slow) {  // rare: the full contract per token, in the slow tokens' lanes only
+    if (kSeq) {  // the lane may leave its sequence below: its pending sums go with it
+      st.seq_x += __double2ll_rn(fa.seq);
+      st.seq_t += fa.seq_t;
+      fa.seq = 0.0;
+      fa.seq_t = 0;
+    }
+    const float num[4] = {numv.x, numv.y, numv.z, numv.w};
+    const float den[4] = {denv.x, denv.y, denv.z, denv.w};
+    (void)num;
+    (void)den;
+#pragma unroll
+    for (int k = 0; k < kTpl; ++k) {
+      if (!((slow >> k) & 1u)) continue;
+      const long long i = i0 + k;
+      if (i >= p.n) continue;
+      const long long g = p.tok_begin + i;
+      const double d = dv[k];
+      if (kSeq) {
+        while (g >= st.next_b) {  // crossed into a later sequence (skips empty ones)
+          SeqAcc a;
+          a.sid = st.sid;
+          a.x = st.seq_x;
+          a.t = st.seq_t;
+          a.nsat = st.seq_nsat;
+          flush_seq(p.seqp, a);
+          st.seq_x = 0;
+          st.seq_nsat = 0;
+          st.seq_t = 0;
+          st.sid += 1;
+          st.next_b = __ldg(p.cu + st.sid + 1);
+        }
+      }
+      if (!isfinite(d)) {  // C.3.2 data error: excluded from every sum, outputs NaN / 0
+        const unsigned long long b = kBadSentinel - static_cast<unsigned long long>(g);
+        st.bad_inv = b > st.bad_inv ? b : st.bad_inv;
+        w_out[k] = CUDART_NAN_F;
+        c_out[k] = 0.f;
+        kbits &= ~(0xffu << (8 * k));
+        continue;
+      }
+      const bool resp = (resp_bits >> (8 * k)) & 0xffu;
+      const bool sm = fabs(d) <= kSmall;
+      double k3, e;
+      if (sm) {
+        k3 = k3s[k];
+        e = exp_from_k3_small(d, k3);
+      } else {
+        const double2 ke = k3_exp_full(d);
+        k3 = ke.x;
+        e = ke.y;
+      }
+      const bool trunc = kTis && d > cfg.log_tis_cap;
+      if (kTis) w_out[k] = __double2float_rn(trunc ? cfg.tis_cap : fmin(e, cfg.tis_cap));
+      const bool keep = kTokRs ? (cfg.log_lo <= d && d <= cfg.log_hi) : true;
+      c_out[k] = (resp && keep) ? w_out[k] : 0.f;
+      kbits = (kbits & ~(0xffu << (8 * k))) | (static_cast<uint32_t>(keep) << (8 * k));
+      if (!resp) continue;
+      bool sat1, sat3;
+      const long long x1 = fixed_point(-d, sat1);
+      const long long x3 = fixed_point(k3, sat3);
+      st.c_resp += 1;
+      st.c_trunc += trunc ? 1u : 0u;
+      st.c_rej += keep ? 0u : 1u;
+      st.s_abs += x1 < 0 ? -x1 : x1;  // rint is odd-symmetric: X(|delta|) = |X(-delta)|
+      st.s_k1 += x1;
+      st.s_k3 += x3;
+      st.mx = fmax(st.mx, fabs(d));
+      if (kSeq && keep) {
+        const bool satq = seq_k1 ? sat1 : sat3;
+        st.seq_x += seq_k1 ? x1 : x3;
+        st.seq_t += 1;
+        st.seq_nsat += satq ? 1 : 0;
+        st.c_sat += satq ? 1 : 0;
+      }
+    }
+  }
+  if (kOut) store_chunk(p, i0, full, w_out, c_out, kbits);
+}
+
+// Pass 1 (a5).  Every warp owns a contiguous run of 128-token chunks (four tokens per lane).
+// The warp streams its chunks' num / den through a kStages-deep ring in shared memory (1-D bulk
+// copies issued by lane 0, completion on one mbarrier per stage), so the bytes in flight do not
+// cost registers; the response mask (128 B per chunk) is prefetched one chunk ahead in a register.
+// Clean chunks (see chunk_body) take the select-free body, the others the masked one.
+template <bool kOut, int kSeqK, bool kTis, bool kTokRs>
+__global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_kernel(LocalParams p) {
+  constexpr bool kSeq = kSeqK != TIM_SEQ_NONE;  // kSeqK: the sequence score (TIM_SEQ_K1 / TIM_SEQ_K3)
+  __shared__ LaneState sh_state[kLocalThreads];
+  __shared__ __align__(128) float ring[kLocalWarps][kStages][2][kWarpTok];
+  __shared__ __align__(8) uint64_t ring_bar[kLocalWarps][kStages];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const long long warp_g = (static_cast<long long>(blockIdx.x) * kLocalThreads + threadIdx.x) >> 5;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * kLocalThreads) >> 5;
+  const long long n_chunks = (p.n + kWarpTok - 1) / kWarpTok;
+  LaneState& st = sh_state[threadIdx.x];
+  st.s_abs = 0;
+  st.s_k1 = 0;
+  st.s_k3 = 0;
+  st.seq_x = 0;
+  st.bad_inv = 0;
+  st.c_sat = 0;
+  st.seq_nsat = 0;
+  st.sid = LLONG_MAX;
+  st.next_b = LLONG_MAX;
+  st.seq_t = 0;
+  st.mx = 0.0;
+  st.c_resp = st.c_trunc = st.c_rej = 0;
+
+  const long long cpw = (n_chunks + nwarps - 1) / nwarps;
+  const long long c_begin = warp_g * cpw;
+  const long long c_end = c_begin + cpw < n_chunks ? c_begin + cpw : n_chunks;
+  long long seq_lim = LLONG_MAX;  // a lane chunk at local index i0 >= seq_lim reaches next_b
+  if (kSeq && c_begin < c_end && c_begin * kWarpTok + lane * kTpl < p.n) {
+    st.sid = seq_of(p.cu, p.n_seq, p.tok_begin + c_begin * kWarpTok + lane * kTpl);
+    st.next_b = __ldg(p.cu + st.sid + 1);
+    seq_lim = st.next_b - p.tok_begin - (kTpl - 1);
+  }
+
+  FastAcc fa;
+  fa.k1 = fa.k3 = fa.ab = fa.seq = fa.mx = 0.0;
+  fa.resp = fa.trunc = fa.rej = fa.seq_t = 0;
+  auto fold = [&]() {  // fp64 sums -> int128
+    st.s_abs += __double2ll_rn(fa.ab);
+    st.s_k1 += __double2ll_rn(fa.k1);
+    st.s_k3 += __double2ll_rn(fa.k3);
+    if (kSeq) st.seq_x += __double2ll_rn(fa.seq);
+    fa.ab = fa.k1 = fa.k3 = fa.seq = 0.0;
+  };
+
+  const long long n_vec = p.vec ? p.n / kWarpTok : 0;  // whole, vector-accessible chunks
+  long long c_mid = c_end < n_vec ? c_end : n_vec;
+  if (c_mid < c_begin) c_mid = c_begin;
+  const uint32_t ring0 = smem_u32(&ring[wib][0][0][0]);
+  const uint32_t bar0 = smem_u32(&ring_bar[wib][0]);
+  const uint64_t pol = policy_evict_first();
+  if (lane == 0) {
+    for (int j = 0; j < kStages; ++j) mbar_init(bar0 + 8 * j, 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  auto issue = [&](int j, long long c) {  // lane 0: chunk c into stage j
+    const uint32_t dst = ring0 + j * (2 * kWarpTok * 4);
+    mbar_arrive_expect_tx(bar0 + 8 * j, 2 * kWarpTok * 4);
+    bulk_g2s(dst, p.num + c * kWarpTok, kWarpTok * 4, bar0 + 8 * j, pol);
+    bulk_g2s(dst + kWarpTok * 4, p.den + c * kWarpTok, kWarpTok * 4, bar0 + 8 * j, pol);
+  };
+  if (lane == 0)
+    for (int j = 0; j < kStages; ++j)
+      if (c_begin + j < c_mid) issue(j, c_begin + j);
+  uint32_t r_nxt = 0x01010101u;
+  if (c_begin < c_mid && p.resp)
+    r_nxt = __ldcs(reinterpret_cast<const unsigned int*>(p.resp + c_begin * kWarpTok + lane * kTpl));
+  int cnt = 0, j = 0;
+  uint32_t phase = 0;
+  for (long long c = c_begin; c < c_mid; ++c) {
+    const long long i0 = c * kWarpTok + lane * kTpl;
+    mbar_wait(bar0 + 8 * j, phase);
+    const float4 numv = *reinterpret_cast<const float4*>(&ring[wib][j][0][lane * kTpl]);
+    const float4 denv = *reinterpret_cast<const float4*>(&ring[wib][j][1][lane * kTpl]);
+    const uint32_t resp = r_nxt;
+    if (c + 1 < c_mid && p.resp) r_nxt = __ldcs(reinterpret_cast<const unsigned int*>(p.resp + i0 + kWarpTok));
+    double dv[kTpl];
+    dv[0] = __dsub_rn(static_cast<double>(numv.x), static_cast<double>(denv.x));
+    dv[1] = __dsub_rn(static_cast<double>(numv.y), static_cast<double>(denv.y));
+    dv[2] = __dsub_rn(static_cast<double>(numv.z), static_cast<double>(denv.z));
+    dv[3] = __dsub_rn(static_cast<double>(numv.w), static_cast<double>(denv.w));
+    __syncwarp();  // every lane has read stage j: refill it with chunk c + kStages
+    if (lane == 0 && c + kStages < c_mid) {
+      fence_proxy_async_smem();
+      issue(j, c + kStages);
+    }
+    if (++j == kStages) {
+      j = 0;
+      phase ^= 1u;
+    }
+    const bool lane_whole = !(kSeq && i0 >= seq_lim);
+    bool lane_fast = lane_whole;
+#pragma unroll
+    for (int k = 0; k < kTpl; ++k) lane_fast = lane_fast && fabs(dv[k]) <= kSmall;  // false for NaN
+    const bool f_all = __all_sync(0xffffffffu, lane_fast && resp == 0x01010101u);
+    const bool f_none = !f_all && __all_sync(0xffffffffu, lane_fast && resp == 0u);
+    if (f_all || f_none) {  // warp-uniform
+      chunk_body<false, kOut, kSeqK, kTis, kTokRs>(p, st, fa, numv, denv, resp, i0, true, true, f_all, dv);
+    } else {
+      chunk_body<true, kOut, kSeqK, kTis, kTokRs>(p, st, fa, numv, denv, resp, i0, true, lane_whole, true, dv);
+      if (kSeq) seq_lim = st.next_b - p.tok_begin - (kTpl - 1);
+    }
+    if (++cnt == kFoldChunks) {
+      fold();
+      cnt = 0;
+    }
+  }
+  // unaligned arrays, or the partial last chunk: element-wise loads, the masked body
+  for (long long ch = c_mid; ch < c_end; ++ch) {
+    const long long i0 = ch * kWarpTok + lane * kTpl;
+    const Chunk cc = load_chunk(p, i0);
+    const bool full = p.vec && i0 + kTpl <= p.n;
+    double dv[kTpl];
+    dv[0] = __dsub_rn(static_cast<double>(cc.num.x), static_cast<double>(cc.den.x));
+    dv[1] = __dsub_rn(static_cast<double>(cc.num.y), static_cast<double>(cc.den.y));
+    dv[2] = __dsub_rn(static_cast<double>(cc.num.z), static_cast<double>(cc.den.z));
+    dv[3] = __dsub_rn(static_cast<double>(cc.num.w), static_cast<double>(cc.den.w));
+    const bool lane_whole = full && !(kSeq && i0 >= seq_lim);
+    chunk_body<true, kOut, kSeqK, kTis, kTokRs>(p, st, fa, cc.num, cc.den, cc.resp, i0, full, lane_whole, true, dv);
+    if (kSeq) seq_lim = st.next_b - p.tok_begin - (kTpl - 1);
+    fold();
+  }
+  fold();
+  st.mx = fa.mx > st.mx ? fa.mx : st.mx;
+  st.c_resp += fa.resp;
+  st.c_trunc += fa.trunc;
+  st.c_rej += fa.rej;
+  st.seq_t += fa.seq_t;
+
+  __int128 s_abs = st.s_abs, s_k1 = st.s_k1, s_k3 = st.s_k3;
+  unsigned long long maxbits = static_cast<unsigned long long>(__double_as_longlong(st.mx));
+  unsigned long long bad_inv = st.bad_inv;
+  long long c_sat = st.c_sat;
+  const unsigned c_resp_t = st.c_resp, c_trunc_t = st.c_trunc, c_rej_t = st.c_rej;
 
   if (kSeq) {
     SeqAcc acc;
-    acc.sid = sid;
-    acc.x = sa.seq_x + static_cast<__int128>(f_seq);
-    acc.t = seq_t;
-    acc.nsat = sa.seq_nsat;
+    acc.sid = st.sid;
+    acc.x = st.seq_x;
+    acc.t = st.seq_t;
+    acc.nsat = st.seq_nsat;
     // segmented warp reduction of the open segments (sequence ids are non-decreasing in lane order)
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -316,9 +456,9 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
   __shared__ long long sh_sum[6][kLocalThreads / 32];
   __shared__ unsigned long long sh_max[kLocalThreads / 32], sh_bad[kLocalThreads / 32];
   const int w = threadIdx.x >> 5;
-  const long long n_resp = warp_sum_i64(static_cast<long long>(c_resp));
-  const long long n_trunc = warp_sum_i64(static_cast<long long>(c_trunc));
-  const long long n_rej = warp_sum_i64(static_cast<long long>(c_rej));
+  const long long n_resp = warp_sum_i64(static_cast<long long>(c_resp_t));
+  const long long n_trunc = warp_sum_i64(static_cast<long long>(c_trunc_t));
+  const long long n_rej = warp_sum_i64(static_cast<long long>(c_rej_t));
   c_sat = warp_sum_i64(c_sat);
   s_abs = warp_sum_i128(s_abs);
   s_k1 = warp_sum_i128(s_k1);
@@ -375,35 +515,61 @@ __global__ void __launch_bounds__(kFinishThreads) correct_finish_kernel(FinishPa
   const CorrectDevCfg cfg = p.cfg;
   __shared__ int sh_rej[kFinishThreads / 32];
   int rej = 0;
-  for (long long s = threadIdx.x; s < p.n_seq; s += blockDim.x) {
-    __int128 X = 0;
-    long long T = 0, nsat = 0;
-    for (int r = 0; r < p.nranks; ++r) {  // fixed rank order (exact anyway)
-      const tim_seq_partial* sp = reinterpret_cast<const tim_seq_partial*>(
-          p.gathered + r * p.block_bytes + sizeof(tim_partial_header)) + s;
-      X += ld_i128(&sp->x_lo);
-      T += sp->n_tok;
-      nsat += sp->n_sat;
+  constexpr int kU = 4;  // sequences per thread per round: their partial loads are issued together
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long s0 = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; s0 < p.n_seq; s0 += kU * stride) {
+    __int128 X[kU];
+    long long T[kU], nsat[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const long long s = s0 + u * stride;
+      X[u] = 0;
+      T[u] = nsat[u] = 0;
+      if (s >= p.n_seq) continue;
+      for (int r = 0; r < p.nranks; ++r) {  // fixed rank order (exact anyway)
+        const tim_seq_partial* sp = reinterpret_cast<const tim_seq_partial*>(
+            p.gathered + r * p.block_bytes + sizeof(tim_partial_header)) + s;
+        const longlong2 xv = *reinterpret_cast<const longlong2*>(sp);       // {x_lo, x_hi}
+        const longlong2 tv = *(reinterpret_cast<const longlong2*>(sp) + 1);  // {n_tok, n_sat}
+        X[u] += (static_cast<__int128>(xv.y) << 64) | static_cast<__int128>(static_cast<unsigned long long>(xv.x));
+        T[u] += tv.x;
+        nsat[u] += tv.y;
+      }
     }
-    uint8_t keep = 1;
-    double score = 0.0;
-    if (cfg.seq_rs != TIM_SEQ_NONE) {
-      score = __dmul_rn(i128_to_double(X), 0x1p-52);
-      if (cfg.seq_agg == TIM_AGG_MEAN) score = T > 0 ? __ddiv_rn(score, static_cast<double>(T)) : 0.0;
-      if (T == 0) keep = 1;
-      else if (nsat > 0) keep = 0;
-      else keep = X <= seq_threshold(cfg.tau_seq, cfg.seq_agg == TIM_AGG_MEAN ? T : 1) ? 1 : 0;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const long long s = s0 + u * stride;
+      if (s >= p.n_seq) continue;
+      uint8_t keep = 1;
+      double score = 0.0;
+      if (cfg.seq_rs != TIM_SEQ_NONE) {
+        score = __dmul_rn(i128_to_double(X[u]), 0x1p-52);
+        if (cfg.seq_agg == TIM_AGG_MEAN) score = T[u] > 0 ? __ddiv_rn(score, static_cast<double>(T[u])) : 0.0;
+        keep = seq_keep_decision(cfg.tau_seq, cfg.seq_agg, X[u], T[u], nsat[u]) ? 1 : 0;
+      }
+      rej += keep ? 0 : 1;
+      if (p.seq_keep) p.seq_keep[s] = keep;
+      if (p.seq_score) p.seq_score[s] = score;
     }
-    rej += keep ? 0 : 1;
-    if (p.seq_keep) p.seq_keep[s] = keep;
-    if (p.seq_score) p.seq_score[s] = score;
   }
   for (int off = 16; off > 0; off >>= 1) rej += __shfl_down_sync(0xffffffffu, rej, off);
   if ((threadIdx.x & 31) == 0) sh_rej[threadIdx.x >> 5] = rej;
   __syncthreads();
-  if (threadIdx.x == 0 && p.stats) {
-    long long n_rej = 0;
-    for (int i = 0; i < kFinishThreads / 32; ++i) n_rej += sh_rej[i];
+  // several blocks (p.scratch = {ticket, rejections}, zeroed): the last block to finish writes the stats
+  __shared__ int last;
+  long long n_rej = 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < static_cast<int>(blockDim.x) / 32; ++i) n_rej += sh_rej[i];
+    last = 1;
+    if (gridDim.x > 1) {
+      atomicAdd(&p.scratch[1], static_cast<unsigned long long>(n_rej));
+      __threadfence();
+      last = atomicAdd(&p.scratch[0], 1ull) == gridDim.x - 1;
+      if (last) n_rej = static_cast<long long>(atomicAdd(&p.scratch[1], 0ull));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && last && p.stats) {
     long long cnt[5] = {0, 0, 0, 0, 0};
     __int128 sums[3] = {0, 0, 0};
     unsigned long long mx = 0;
@@ -460,27 +626,36 @@ cudaError_t launch_correct_local(const LocalParams& p, int num_sms, cudaStream_t
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   const bool out = p.tis_w != nullptr;
-  const bool seq = p.cfg.seq_rs != TIM_SEQ_NONE;
-  const int v = (out ? 8 : 0) | (seq ? 4 : 0) | (p.cfg.tis ? 2 : 0) | (p.cfg.tok_rs ? 1 : 0);
+  const int sk = p.cfg.seq_rs;
+  const int v = (out ? 8 : 0) | (p.cfg.tis ? 2 : 0) | (p.cfg.tok_rs ? 1 : 0);
+#define TIM_CORR_CASE(o, t, r)                                                                   \
+  case (o ? 8 : 0) | (t ? 2 : 0) | (r ? 1 : 0):                                                  \
+    if (sk == TIM_SEQ_K1)                                                                        \
+      correct_local_kernel<o, TIM_SEQ_K1, t, r><<<blocks, kLocalThreads, 0, stream>>>(p);        \
+    else if (sk == TIM_SEQ_K3)                                                                   \
+      correct_local_kernel<o, TIM_SEQ_K3, t, r><<<blocks, kLocalThreads, 0, stream>>>(p);        \
+    else                                                                                         \
+      correct_local_kernel<o, TIM_SEQ_NONE, t, r><<<blocks, kLocalThreads, 0, stream>>>(p);      \
+    break;
   switch (v) {
-#define TIM_CORR_CASE(o, s, t, r) \
-  case (o ? 8 : 0) | (s ? 4 : 0) | (t ? 2 : 0) | (r ? 1 : 0): \
-    correct_local_kernel<o, s, t, r><<<blocks, kLocalThreads, 0, stream>>>(p); break;
-    TIM_CORR_CASE(true, true, true, true) TIM_CORR_CASE(true, true, true, false)
-    TIM_CORR_CASE(true, true, false, true) TIM_CORR_CASE(true, true, false, false)
-    TIM_CORR_CASE(true, false, true, true) TIM_CORR_CASE(true, false, true, false)
-    TIM_CORR_CASE(true, false, false, true) TIM_CORR_CASE(true, false, false, false)
-    TIM_CORR_CASE(false, true, true, true) TIM_CORR_CASE(false, true, true, false)
-    TIM_CORR_CASE(false, true, false, true) TIM_CORR_CASE(false, true, false, false)
-    TIM_CORR_CASE(false, false, true, true) TIM_CORR_CASE(false, false, true, false)
-    TIM_CORR_CASE(false, false, false, true) TIM_CORR_CASE(false, false, false, false)
-#undef TIM_CORR_CASE
+    TIM_CORR_CASE(true, true, true) TIM_CORR_CASE(true, true, false)
+    TIM_CORR_CASE(true, false, true) TIM_CORR_CASE(true, false, false)
+    TIM_CORR_CASE(false, true, true) TIM_CORR_CASE(false, true, false)
+    TIM_CORR_CASE(false, false, true) TIM_CORR_CASE(false, false, false)
   }
+#undef TIM_CORR_CASE
   return cudaGetLastError();
 }
 
-cudaError_t launch_correct_finish(const FinishParams& p, cudaStream_t stream) {
-  correct_finish_kernel<<<1, kFinishThreads, 0, stream>>>(p);
+cudaError_t launch_correct_finish(const FinishParams& p, int num_sms, cudaStream_t stream) {
+  if (p.scratch == nullptr) {  // no zeroed scratch: one block
+    correct_finish_kernel<<<1, kFinishThreads, 0, stream>>>(p);
+  } else {
+    long long blocks = (p.n_seq + 255) / 256;
+    if (blocks > num_sms) blocks = num_sms;
+    if (blocks < 1) blocks = 1;
+    correct_finish_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(p);
+  }
   return cudaGetLastError();
 }
 

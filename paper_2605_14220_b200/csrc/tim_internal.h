@@ -145,6 +145,7 @@ struct FinishParams {
   uint8_t* seq_keep;     // may be null
   double* seq_score;     // may be null
   tim_stats* stats;      // may be null
+  unsigned long long* scratch;  // {ticket, rejections}, zeroed, or null (then one block)
 };
 struct ZeroParams {
   const int64_t* cu;
@@ -203,7 +204,7 @@ cudaError_t launch_ppo_local(const PpoLocalParams& p, int num_sms, cudaStream_t 
 cudaError_t launch_ppo_finish(const PpoFinishParams& p, cudaStream_t stream);
 
 cudaError_t launch_correct_local(const LocalParams& p, int num_sms, cudaStream_t stream);
-cudaError_t launch_correct_finish(const FinishParams& p, cudaStream_t stream);
+cudaError_t launch_correct_finish(const FinishParams& p, int num_sms, cudaStream_t stream);
 cudaError_t launch_correct_zero(const ZeroParams& p, cudaStream_t stream);
 
 }  // namespace tim
