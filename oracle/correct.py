@@ -22,8 +22,10 @@ multiply-add: numpy never fuses separate ufunc calls).
            token keep <=> ln lo <= delta <= ln hi               (reading U4)
   C.3.5  K1 = -delta
   C.3.6  K3 = k3_c(delta): |delta| <= 1: delta^2 * P(delta), P the Horner
-         series of (e^x - 1 - x)/x^2 with coefficients RN(1/n!), n = 2..23;
-         otherwise (exp_c(delta) - 1) - delta, exp_c = Cody-Waite reduction
+         series of (e^x - 1 - x)/x^2 with coefficients RN(1/n!), n = 2..9 for
+         |delta| <= 2^-6, 2..15 for |delta| <= 2^-2, 2..23 for |delta| <= 1;
+         otherwise (exp_c(delta) - 1) - delta.  exp_c = (1 + delta) + K3 for
+         |delta| <= 2^-2 (same series), else Cody-Waite reduction
          k = rint(delta * log2 e), r = (delta - k*ln2_hi) - k*ln2_lo, degree-13
          Taylor Horner on r, then ldexp(., k); exp_c = +inf for delta > 709,
          0 for delta < -700.
@@ -86,12 +88,21 @@ def delta(lp_num, lp_den) -> np.ndarray:
         np.asarray(lp_den, dtype=np.float32).astype(np.float64)
 
 
-SMALL = 2.0 ** -6  # |delta| <= SMALL: short Horner polynomials (truncation < 1e-19 relative)
+SMALL = 2.0 ** -6  # |delta| <= SMALL: short Horner polynomial n = 2..9 (truncation < 1e-19 relative)
+MID = 2.0 ** -2    # |delta| <= MID:   n = 2..15 (first dropped term < 4e-22 relative)
+
+
+def _k3_series(d, top: int) -> np.ndarray:
+    """d^2 Q(d), Q = Horner of (e^x - 1 - x)/x^2 with coefficients RN(1/n!), n = top..2."""
+    Q = np.full_like(d, INV_FACT[top])
+    for n in range(top - 1, 1, -1):
+        Q = Q * d + INV_FACT[n]
+    return (d * d) * Q
 
 
 def exp_contract(d) -> np.ndarray:
-    """C.3.6 exp_c.  |d| <= 2^-6: (1 + d) + K3_small(d), K3_small = d^2 Q(d) the short
-    series of k3_contract (n = 2..9), i.e. e^d = 1 + d + (e^d - 1 - d).  Otherwise Cody-Waite
+    """C.3.6 exp_c.  |d| <= 2^-2: (1 + d) + K3_series(d) with the K3 branch's own series (n = 2..9
+    for |d| <= 2^-6, n = 2..15 above), i.e. e^d = 1 + d + (e^d - 1 - d).  Otherwise Cody-Waite
     reduction + degree-13 Taylor Horner + ldexp; +inf above 709, 0 below -700."""
     d = np.asarray(d, dtype=np.float64)
     dd = np.where(np.isfinite(d), np.clip(d, -700.0, 709.0), 0.0)
@@ -102,11 +113,11 @@ def exp_contract(d) -> np.ndarray:
         p = p * r + INV_FACT[n]
     out = np.ldexp(p, k.astype(np.int64))
     small = np.abs(dd) <= SMALL
+    mid = ~small & (np.abs(dd) <= MID)
     ds = np.where(small, dd, 0.0)
-    Q = np.full_like(ds, INV_FACT[9])
-    for n in range(8, 1, -1):
-        Q = Q * ds + INV_FACT[n]
-    out = np.where(small, (1.0 + ds) + (ds * ds) * Q, out)
+    dm = np.where(mid, dd, 0.0)
+    out = np.where(mid, (1.0 + dm) + _k3_series(dm, 15), out)
+    out = np.where(small, (1.0 + ds) + _k3_series(ds, 9), out)
     out = np.where(d > 709.0, np.inf, out)
     out = np.where(d < -700.0, 0.0, out)
     return out
@@ -114,22 +125,18 @@ def exp_contract(d) -> np.ndarray:
 
 def k3_contract(d) -> np.ndarray:
     """C.3.6 K3 = e^d - 1 - d = d^2 P(d): P = Horner series of RN(1/n!) with n = 2..9 for
-    |d| <= 2^-6 and n = 2..23 for |d| <= 1; (exp_c(d) - 1) - d otherwise."""
+    |d| <= 2^-6, n = 2..15 for |d| <= 2^-2 and n = 2..23 for |d| <= 1; (exp_c(d) - 1) - d
+    otherwise."""
     d = np.asarray(d, dtype=np.float64)
-    small = np.abs(d) <= 1.0
-    ds = np.where(small, d, 0.0)
-    P = np.full_like(ds, INV_FACT[23])
-    for n in range(22, 1, -1):
-        P = P * ds + INV_FACT[n]
-    series = (ds * ds) * P
-    tiny = np.abs(d) <= SMALL
-    dt = np.where(tiny, d, 0.0)
-    Q = np.full_like(dt, INV_FACT[9])
-    for n in range(8, 1, -1):
-        Q = Q * dt + INV_FACT[n]
-    series = np.where(tiny, (dt * dt) * Q, series)
-    big = (exp_contract(d) - 1.0) - d
-    return np.where(small, series, big)
+    ad = np.abs(d)
+    tiny = ad <= SMALL
+    mid = ~tiny & (ad <= MID)
+    med = ~tiny & ~mid & (ad <= 1.0)
+    out = (exp_contract(d) - 1.0) - d
+    out = np.where(med, _k3_series(np.where(med, d, 0.0), 23), out)
+    out = np.where(mid, _k3_series(np.where(mid, d, 0.0), 15), out)
+    out = np.where(tiny, _k3_series(np.where(tiny, d, 0.0), 9), out)
+    return out
 
 
 def fixed_point(K) -> tuple[np.ndarray, np.ndarray]:

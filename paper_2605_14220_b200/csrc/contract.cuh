@@ -28,21 +28,32 @@ constexpr double kLn2Lo = 0x1.a39ef35793c76p-33;
 constexpr double kTwo52 = 0x1p52;
 constexpr long long kSatX = 1ll << 62;
 
-constexpr double kSmall = 0x1p-6;  // |d| <= 2^-6: short Horner polynomials
+constexpr double kSmall = 0x1p-6;  // |d| <= 2^-6: short Horner polynomial (n = 2..9)
+constexpr double kMid = 0x1p-2;    // |d| <= 2^-2: n = 2..15
 
-// Short K3 series for |d| <= 2^-6: d^2 Q(d), Q = Horner of RN(1/n!), n = 2..9.
-__device__ __forceinline__ double k3_small(double d) {
-  double Q = kInvFact[9];
+// K3 series d^2 Q(d), Q = Horner of RN(1/n!), n = kTop..2.
+template <int kTop>
+__device__ __forceinline__ double k3_series(double d) {
+  double Q = kInvFact[kTop];
 #pragma unroll
-  for (int n = 8; n >= 2; --n) Q = __dadd_rn(__dmul_rn(Q, d), kInvFact[n]);
+  for (int n = kTop - 1; n >= 2; --n) Q = __dadd_rn(__dmul_rn(Q, d), kInvFact[n]);
   return __dmul_rn(__dmul_rn(d, d), Q);
 }
+__device__ __forceinline__ double k3_small(double d) { return k3_series<9>(d); }
+__device__ __forceinline__ double k3_mid(double d) { return k3_series<15>(d); }
+__device__ __forceinline__ double k3_medium(double d) { return k3_series<23>(d); }
 
-// Medium K3 series for |d| <= 1: d^2 P(d), P = Horner of RN(1/n!), n = 2..23.
-__device__ __forceinline__ double k3_medium(double d) {
-  double P = kInvFact[23];
+// The short and mid series of one token in a single Horner chain: the mid prefix (n = 15..10)
+// runs for every token, then a tiny token (|d| <= 2^-6) restarts from RN(0 * d + c9) = c9, which
+// is exactly the short series' start; n = 8..2 are the same ops for both.  Bit-identical to
+// k3_small (tiny) / k3_mid (otherwise).
+__device__ __forceinline__ double k3_small_or_mid(double d, bool tiny) {
+  double P = kInvFact[15];
 #pragma unroll
-  for (int n = 22; n >= 2; --n) P = __dadd_rn(__dmul_rn(P, d), kInvFact[n]);
+  for (int n = 14; n >= 10; --n) P = __dadd_rn(__dmul_rn(P, d), kInvFact[n]);
+  P = __dadd_rn(__dmul_rn(tiny ? 0.0 : P, d), kInvFact[9]);
+#pragma unroll
+  for (int n = 8; n >= 2; --n) P = __dadd_rn(__dmul_rn(P, d), kInvFact[n]);
   return __dmul_rn(__dmul_rn(d, d), P);
 }
 
@@ -58,21 +69,24 @@ __device__ __forceinline__ double exp_cw(double d) {
   return __dmul_rn(p, __longlong_as_double((ki + 1023) << 52));
 }
 
-// e^d.  |d| <= 2^-6: (1 + d) + k3_small(d) (e^d = 1 + d + K3, the K3 the caller needs anyway).
-// Otherwise Cody-Waite (exp_cw); +inf above 709, 0 below -700.
+// e^d.  |d| <= 2^-2: (1 + d) + K3(d) with the K3 branch's own series (e^d = 1 + d + K3, the K3
+// the caller needs anyway).  Otherwise Cody-Waite (exp_cw); +inf above 709, 0 below -700.
 __device__ __forceinline__ double exp_from_k3_small(double d, double k3s) { return __dadd_rn(__dadd_rn(1.0, d), k3s); }
 __device__ __forceinline__ double exp_c(double d) {
   if (d > 709.0) return CUDART_INF;
   if (d < -700.0) return 0.0;
-  if (fabs(d) <= kSmall) return exp_from_k3_small(d, k3_small(d));
+  const double ad = fabs(d);
+  if (ad <= kSmall) return exp_from_k3_small(d, k3_small(d));
+  if (ad <= kMid) return exp_from_k3_small(d, k3_mid(d));
   return exp_cw(d);
 }
 
 // K3 = e^d - 1 - d = d^2 P(d): Horner series of (e^d - 1 - d) / d^2 with RN(1/n!), n = 2..9 for
-// |d| <= 2^-6 (k3_small), n = 2..23 for |d| <= 1 (k3_medium); (exp_c(d) - 1) - d otherwise.
+// |d| <= 2^-6, n = 2..15 for |d| <= 2^-2, n = 2..23 for |d| <= 1; (exp_c(d) - 1) - d otherwise.
 __device__ __forceinline__ double k3_c(double d) {
   const double ad = fabs(d);
   if (ad <= kSmall) return k3_small(d);
+  if (ad <= kMid) return k3_mid(d);
   if (ad <= 1.0) return k3_medium(d);
   return __dsub_rn(__dsub_rn(exp_c(d), 1.0), d);
 }

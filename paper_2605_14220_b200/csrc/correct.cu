@@ -105,7 +105,13 @@ __device__ __forceinline__ void store_chunk(const LocalParams& p, long long i0, 
 
 // K3 and e^delta of a token outside the short-polynomial range (rare; out of line so the
 // chunk loop keeps its registers and stays in the instruction cache).
-__device__ __noinline__ double2 k3_exp_full(double d) { return make_double2(k3_c(d), exp_c(d)); }
+__device__ __noinline__ double2 k3_exp_full(double d) {
+  if (fabs(d) <= kMid) {  // series branches: e^d = (1 + d) + K3 with the same series
+    const double k3 = fabs(d) <= kSmall ? k3_small(d) : k3_mid(d);
+    return make_double2(k3, exp_from_k3_small(d, k3));
+  }
+  return make_double2(k3_c(d), exp_c(d));
+}
 
 // Fast-path register state of a lane: exact fp64 sums of quantised values (each an integer with
 // |X| <= 2^46, so 16 chunks of four sum exactly, < 2^52), max |delta| and counters.

@@ -69,11 +69,11 @@ __device__ __forceinline__ int hist_slot(const PpoLocalParams& p, double r, doub
   return raw < 0.0 ? 0 : (raw >= static_cast<double>(p.bins) ? p.bins + 1 : static_cast<int>(raw) + 1);
 }
 
-// Same structure as correct_local_kernel: 4 tokens per lane, next chunk prefetched, a lock-step
-// fast path (|delta| <= 1, |loss| <= 2^8: contract polynomials in lock-step, exact int64 chunk
-// sums folded into int128 per chunk) and a rare per-lane slow path with the full contract
-// (larger delta or loss, non-finite input, partial or unaligned chunk, sequence boundary inside
-// the lane's tokens).
+// 4 tokens per lane, next chunk prefetched, a lock-step fast path (|delta| <= 2^-2, |loss| <=
+// 2^8: the short / mid contract series in one Horner chain per token, exact int64 chunk sums
+// folded into int128 per chunk) and a rare per-lane slow path with the full contract (larger delta
+// or loss, non-finite input, partial or unaligned chunk, sequence boundary inside the lane's
+// tokens).
 __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLocalParams p) {
   extern __shared__ int sh_hist[];  // [2][bins + 2]
   const int nslot = p.bins + 2;
@@ -115,45 +115,20 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
     const float wv_[4] = {cur.w.x, cur.w.y, cur.w.z, cur.w.w};
     const bool full = p.vec && i0 + kPpoTpl <= p.n;
 
-    // fast tokens: |delta| <= 1 (finite).  The short (|delta| <= 2^-6) and the medium contract
-    // branches both run in lock-step over the lane's four tokens (the medium one only when some
-    // lane of the warp needs it), each token then takes its branch's value.
-    double dv[kPpoTpl], ds[kPpoTpl], dm[kPpoTpl], k3s[kPpoTpl], k3m[kPpoTpl], em[kPpoTpl];
+    // fast tokens: |delta| <= 2^-2 (finite): the short (|delta| <= 2^-6) and the mid contract
+    // series in one lock-step Horner chain per token (k3_small_or_mid), e^delta = (1 + delta) + K3.
+    double dv[kPpoTpl], df[kPpoTpl], k3f[kPpoTpl];
     unsigned slow = full ? 0u : 0xFu;
     if (p.tok_begin + i0 + (kPpoTpl - 1) >= next_b) slow = 0xFu;
-    bool any_med = false;
 #pragma unroll
     for (int k = 0; k < kPpoTpl; ++k) {
       dv[k] = __dsub_rn(static_cast<double>(cu_[k]), static_cast<double>(ol_[k]));
-      const double ad = fabs(dv[k]);
-      const bool tiny = ad <= kSmall;  // false for NaN / inf
-      const bool med = !tiny && ad <= 1.0;
-      if (!tiny && !med) slow |= 1u << k;
-      ds[k] = tiny ? dv[k] : 0.0;
-      dm[k] = med ? dv[k] : 0.0;
-      any_med = any_med || med;
+      const bool fast = fabs(dv[k]) <= kMid;  // false for NaN / inf
+      if (!fast) slow |= 1u << k;
+      df[k] = fast ? dv[k] : 0.0;
     }
-    double q[kPpoTpl];
 #pragma unroll
-    for (int k = 0; k < kPpoTpl; ++k) q[k] = kInvFact[9];
-#pragma unroll
-    for (int n = 8; n >= 2; --n)
-#pragma unroll
-      for (int k = 0; k < kPpoTpl; ++k) q[k] = __dadd_rn(__dmul_rn(q[k], ds[k]), kInvFact[n]);
-#pragma unroll
-    for (int k = 0; k < kPpoTpl; ++k) k3s[k] = __dmul_rn(__dmul_rn(ds[k], ds[k]), q[k]);
-    if (__any_sync(0xffffffffu, any_med)) {
-#pragma unroll
-      for (int k = 0; k < kPpoTpl; ++k) k3m[k] = k3_medium(dm[k]);
-#pragma unroll
-      for (int k = 0; k < kPpoTpl; ++k) em[k] = exp_cw(dm[k]);
-    } else {
-#pragma unroll
-      for (int k = 0; k < kPpoTpl; ++k) {
-        k3m[k] = 0.0;
-        em[k] = 1.0;
-      }
-    }
+    for (int k = 0; k < kPpoTpl; ++k) k3f[k] = k3_small_or_mid(df[k], fabs(df[k]) <= kSmall);
 
     float l_out[kPpoTpl], g_out[kPpoTpl];
     uint32_t cbits = 0;
@@ -161,10 +136,9 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
     unsigned cn = 0, ccl = 0, cz = 0;
 #pragma unroll
     for (int k = 0; k < kPpoTpl; ++k) {
-      const bool tiny = fabs(dv[k]) <= kSmall;
-      const double d = tiny ? ds[k] : dm[k];
-      const double k3 = tiny ? k3s[k] : k3m[k];
-      const double r = tiny ? exp_from_k3_small(ds[k], k3s[k]) : em[k];
+      const double d = df[k];
+      const double k3 = k3f[k];
+      const double r = exp_from_k3_small(d, k3);
       const double A = static_cast<double>(ad_[k]);
       const bool clipped = (A > 0.0 && r > p.clip_hi) || (A < 0.0 && r < p.clip_lo);
       const double sv = clipped ? __dmul_rn(A > 0.0 ? p.clip_hi : p.clip_lo, A) : __dmul_rn(r, A);

@@ -76,8 +76,9 @@ def test_table1_without_flip_token_kept(table1, agg):
 def _sweep():
     mags = np.logspace(-300, math.log10(1024.0), 3000)
     extra = np.array([1e-12, 1e-8, 0.5, 0.999999, 1.0, 1.0000001, math.log(2), 6.9, 6.94, 7.0, 709.0, 700.0,
-                      2.0 ** -6, np.nextafter(2.0 ** -6, 1.0), np.nextafter(2.0 ** -6, 0.0)])
-    v = np.concatenate([mags, extra, np.linspace(1e-4, 2.0 ** -5, 700)])
+                      2.0 ** -6, np.nextafter(2.0 ** -6, 1.0), np.nextafter(2.0 ** -6, 0.0),
+                      2.0 ** -2, np.nextafter(2.0 ** -2, 1.0), np.nextafter(2.0 ** -2, 0.0)])
+    v = np.concatenate([mags, extra, np.linspace(1e-4, 2.0 ** -5, 700), np.linspace(2.0 ** -6, 0.3, 700)])
     return np.concatenate([v, -v, [0.0]])
 
 
@@ -99,7 +100,8 @@ def test_k3_contract_within_4_ulp_of_60_digit_reference():
 
 
 def test_exp_contract_within_2_ulp():
-    d = np.concatenate([np.linspace(-700, 709, 4001), np.linspace(-2, 2, 2001)])
+    d = np.concatenate([np.linspace(-700, 709, 4001), np.linspace(-2, 2, 2001), np.linspace(-0.26, 0.26, 2001),
+                        [2.0 ** -2, -(2.0 ** -2), np.nextafter(2.0 ** -2, 1.0), np.nextafter(-(2.0 ** -2), -1.0)]])
     e = oc.exp_contract(d)
     for x, y in zip(d, e):
         ref = float(exact.exp_mp(float(x)))
