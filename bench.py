@@ -111,6 +111,18 @@ def _traffic(config: str):
         return None
 
 
+def _hbm_traffic(key: str, n: int):
+    """dram bytes per pass-1 launch of the correction / PPO kernel at 2^27 tokens, from the
+    committed ncu --set full summary (None for another size or when absent)."""
+    if n != 1 << 27:
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_hbm_kernels_summary.json")) as f:
+            return json.load(f).get(key)
+    except Exception:
+        return None
+
+
 def build_workload(cfg, rank, device):
     seed = cfg.seed + 1000 * rank
     W = synth.head_weight(cfg.vocab, cfg.hidden, cfg.seed, device=device)  # replicated lm_head
@@ -380,7 +392,8 @@ def ppo_roofline(tim, dev, n, peaks, peak_src, reps=10):
     ms = sorted(a.elapsed_time(b) for a, b in evs)[reps // 2]
     gbs = 25.0 * n / (ms / 1e3) / 1e9
     peak = float(peaks["hbm_gbs"])
-    return {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak, "n_tok": n, "ms": ms,
+    return {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+            "traffic": _hbm_traffic("ppo_local_dram_bytes_2e27", n), "n_tok": n, "ms": ms,
             "algorithmic_bytes_per_token": 25, "kernel": "tim_ppo_loss (ppo_local + finish, median of %d)" % reps}
 
 
@@ -413,7 +426,8 @@ def correction_roofline(tim, dev, n, peaks, peak_src, reps=10):
     ms = sorted(a.elapsed_time(b) for a, b in evs)[reps // 2]
     gbs = 18.0 * n / (ms / 1e3) / 1e9
     peak = float(peaks["hbm_gbs"])
-    return {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak, "traffic": None,
+    return {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+            "traffic": _hbm_traffic("correct_local_dram_bytes_2e27", n),
             "n_tok": n, "ms": ms, "algorithmic_bytes_per_token": 18, "peak_source": peak_src + " hbm_gbs",
             "kernel": "tim_correct (correct_local + finish + zero, median of %d)" % reps}
 

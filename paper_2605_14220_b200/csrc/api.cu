@@ -939,8 +939,9 @@ tim_status tim_ppo_local(const float* cur, const float* old, const float* adv, c
   return launch_ppo_local(p, dev->num_sms, s) == cudaSuccess ? TIM_OK : TIM_ERR_CUDA;
 }
 
-tim_status tim_ppo_finish(const void* gathered, int32_t nranks, int64_t n_seq, const tim_ppo_cfg* cfg,
-                          double* seq_loss, int64_t* hist, tim_ppo_stats* stats, void* stream) {
+static tim_status ppo_finish_impl(const void* gathered, int32_t nranks, int64_t n_seq, const tim_ppo_cfg* cfg,
+                                  double* seq_loss, int64_t* hist, tim_ppo_stats* stats, unsigned long long* scratch,
+                                  void* stream) {
   if (!gathered) return TIM_ERR_NULL;
   if (nranks < 1 || n_seq < 0) return TIM_ERR_SHAPE;
   tim_status st = check_ppo_cfg(cfg);
@@ -957,7 +958,14 @@ tim_status tim_ppo_finish(const void* gathered, int32_t nranks, int64_t n_seq, c
   f.seq_loss = seq_loss;
   f.hist = hist;
   f.stats = stats;
-  return launch_ppo_finish(f, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? TIM_OK : TIM_ERR_CUDA;
+  f.scratch = scratch;
+  return launch_ppo_finish(f, dev->num_sms, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? TIM_OK
+                                                                                                   : TIM_ERR_CUDA;
+}
+
+tim_status tim_ppo_finish(const void* gathered, int32_t nranks, int64_t n_seq, const tim_ppo_cfg* cfg,
+                          double* seq_loss, int64_t* hist, tim_ppo_stats* stats, void* stream) {
+  return ppo_finish_impl(gathered, nranks, n_seq, cfg, seq_loss, hist, stats, nullptr, stream);
 }
 
 tim_status tim_ppo_loss(const float* cur, const float* old, const float* adv, const float* coeff, const uint8_t* resp,
@@ -984,7 +992,11 @@ tim_status tim_ppo_loss(const float* cur, const float* old, const float* adv, co
       return TIM_ERR_NCCL;
     gathered = local + blk;
   }
-  return tim_ppo_finish(gathered, nranks, n_seq, cfg, seq_loss, hist, stats, stream);
+  // the local block's header reserved[2..3] (zeroed with the block; pass 1 uses [0..1]) serve as
+  // the finish pass's {ticket, contributing sequences}
+  unsigned long long* scratch =
+      reinterpret_cast<unsigned long long*>(&reinterpret_cast<tim_ppo_partial_header*>(local)->reserved[2]);
+  return ppo_finish_impl(gathered, nranks, n_seq, cfg, seq_loss, hist, stats, scratch, stream);
 }
 
 tim_status tim_ppo_stats_finalize(tim_ppo_stats* h) {

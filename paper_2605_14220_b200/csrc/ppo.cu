@@ -288,7 +288,9 @@ __global__ void __launch_bounds__(kPpoFinishThreads) ppo_finish_kernel(PpoFinish
   long long nc = 0;
   const int nslot = p.bins + 2;
   const int64_t seq_off = static_cast<int64_t>(sizeof(tim_ppo_partial_header)) + 16ll * nslot;
-  for (long long s = threadIdx.x; s < p.n_seq; s += blockDim.x) {
+  const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long s = tid; s < p.n_seq; s += stride) {
     __int128 X = 0;
     long long T = 0;
     for (int r = 0; r < p.nranks; ++r) {
@@ -301,7 +303,7 @@ __global__ void __launch_bounds__(kPpoFinishThreads) ppo_finish_kernel(PpoFinish
     if (p.seq_loss) p.seq_loss[s] = __dmul_rn(i128_to_double(X), 0x1p-52);
   }
   if (p.hist) {
-    for (int i = threadIdx.x; i < 2 * nslot; i += blockDim.x) {
+    for (long long i = tid; i < 2 * nslot; i += stride) {
       long long v = 0;
       for (int r = 0; r < p.nranks; ++r)
         v += reinterpret_cast<const int64_t*>(p.gathered + r * p.block_bytes + sizeof(tim_ppo_partial_header))[i];
@@ -311,9 +313,21 @@ __global__ void __launch_bounds__(kPpoFinishThreads) ppo_finish_kernel(PpoFinish
   for (int off = 16; off > 0; off >>= 1) nc += __shfl_down_sync(0xffffffffu, nc, off);
   if ((threadIdx.x & 31) == 0) sh_nc[threadIdx.x >> 5] = nc;
   __syncthreads();
-  if (threadIdx.x == 0 && p.stats) {
-    long long n_seq_contrib = 0;
-    for (int i = 0; i < kPpoFinishThreads / 32; ++i) n_seq_contrib += sh_nc[i];
+  // several blocks (p.scratch = {ticket, contributing sequences}, zeroed): the last block writes the stats
+  __shared__ int last;
+  long long n_seq_contrib = 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < static_cast<int>(blockDim.x) / 32; ++i) n_seq_contrib += sh_nc[i];
+    last = 1;
+    if (gridDim.x > 1) {
+      atomicAdd(&p.scratch[1], static_cast<unsigned long long>(n_seq_contrib));
+      __threadfence();
+      last = atomicAdd(&p.scratch[0], 1ull) == gridDim.x - 1;
+      if (last) n_seq_contrib = static_cast<long long>(atomicAdd(&p.scratch[1], 0ull));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && last && p.stats) {
     long long cnt[5] = {0, 0, 0, 0, 0};
     __int128 sums[3] = {0, 0, 0};
     for (int r = 0; r < p.nranks; ++r) {
@@ -360,8 +374,15 @@ cudaError_t launch_ppo_local(const PpoLocalParams& p, int num_sms, cudaStream_t 
   return cudaGetLastError();
 }
 
-cudaError_t launch_ppo_finish(const PpoFinishParams& p, cudaStream_t stream) {
-  ppo_finish_kernel<<<1, kPpoFinishThreads, 0, stream>>>(p);
+cudaError_t launch_ppo_finish(const PpoFinishParams& p, int num_sms, cudaStream_t stream) {
+  if (p.scratch == nullptr) {  // no zeroed scratch: one block
+    ppo_finish_kernel<<<1, kPpoFinishThreads, 0, stream>>>(p);
+  } else {
+    long long blocks = (p.n_seq + 255) / 256;
+    if (blocks > num_sms) blocks = num_sms;
+    if (blocks < 1) blocks = 1;
+    ppo_finish_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(p);
+  }
   return cudaGetLastError();
 }
 

@@ -186,6 +186,7 @@ struct PpoFinishParams {
   double* seq_loss;      // may be null
   int64_t* hist;         // may be null
   tim_ppo_stats* stats;  // may be null
+  unsigned long long* scratch;  // {ticket, contributing sequences}, zeroed, or null (then one block)
 };
 int ppo_max_hist_bins();
 
@@ -201,7 +202,7 @@ struct RmsNormParams {
 };
 cudaError_t launch_rmsnorm(const RmsNormParams& p, cudaStream_t stream);
 cudaError_t launch_ppo_local(const PpoLocalParams& p, int num_sms, cudaStream_t stream);
-cudaError_t launch_ppo_finish(const PpoFinishParams& p, cudaStream_t stream);
+cudaError_t launch_ppo_finish(const PpoFinishParams& p, int num_sms, cudaStream_t stream);
 
 cudaError_t launch_correct_local(const LocalParams& p, int num_sms, cudaStream_t stream);
 cudaError_t launch_correct_finish(const FinishParams& p, int num_sms, cudaStream_t stream);
