@@ -21,3 +21,14 @@ res = tim.correct(lp, roll, cu, tim.PRESETS["tis-srs-k3-corr-ratio"], mask)
 pp = tim.ppo_loss(lp, roll, torch.randn(300, device=dev), cu, tim.PPOConfig(), coeff=res["coeff"])
 torch.cuda.synchronize()
 print("sanitize run ok", float(lp.sum()), res["stats"]["n_seq_rejected"], pp["stats"]["n_clipped"])
+# a larger correction / PPO call: several chunks per warp, so the per-warp TMA ring of the
+# correction kernel wraps around (stages refilled), with variable-length sequences
+cu2 = synth.cu_seqlens(256, 16384, variable=True, seed=11).to(dev)
+n2 = int(cu2[-1])
+den2 = -torch.rand(n2, device=dev) * 3
+num2 = synth.perturb_laplace_mix(den2, 12)
+mask2 = (torch.rand(n2, device=dev) > 0.2).to(torch.uint8)
+res2 = tim.correct(num2, den2, cu2, tim.PRESETS["tis-srs-k3-corr-ratio"], mask2)
+pp2 = tim.ppo_loss(num2, den2, torch.randn(n2, device=dev), cu2, tim.PPOConfig(), coeff=res2["coeff"])
+torch.cuda.synchronize()
+print("sanitize large run ok", n2, res2["stats"]["n_seq_rejected"], pp2["stats"]["n_clipped"])
