@@ -227,6 +227,23 @@ def run_ours(args):
     if not torch.equal(a.view(torch.int32), ref_bits):
         max_shape_diff = max(max_shape_diff, (a - lp[samp]).abs().max().item())
 
+    # small-batch latency (rollout-side scoring): one call on the first n rows, n <= one M-tile
+    small = {}
+    for n_small in (1, 64, 256):
+        lps = torch.empty(n_small, device=dev)
+        ens = torch.empty(n_small, device=dev)
+        for _ in range(3):
+            tim.logprob(H[:n_small], W, ids[:n_small], out=(lps, ens))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            tim.logprob(H[:n_small], W, ids[:n_small], out=(lps, ens))
+        e1.record()
+        torch.cuda.synchronize()
+        small[str(n_small)] = round(e0.elapsed_time(e1) / 10, 4)
+        assert torch.equal(lps.view(torch.int32), lp[:n_small].view(torch.int32))  # batch invariance
+
     # NEXT-1 rollout-side twin on the same batch: draw throughput and the zero-mismatch check
     sample_info = None
     if args.sample_bench:
@@ -336,6 +353,8 @@ def run_ours(args):
             "l2": "inputs larger than L2 (H %.2f GB/GPU, W %.2f GB)" % (H_bytes(cfg) / 1e9, W.numel() * 2 / 1e9),
         },
         "max_abs_dlogp_across_shapes": max_shape_diff,
+        "small_batch_latency_ms": {"n_tok": small, "note": "tim_logprob on the first n rows of the batch, "
+                                   "bitwise equal to their logp in the full batch"},
         "gpu_launches": KERNELS_PER_STEP * args.steps,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "frac_of_burst": achieved / float(peaks["bf16_tflops"]),

@@ -106,7 +106,10 @@ tim_status tim_logprob(const void* hidden_bf16, int64_t ld_hidden,
                        void* workspace, size_t workspace_bytes,
                        tim_device_status* dstatus, void* stream);
 
-/* Number of vocab slices S_v of the fixed split for a given vocab (numerics contract, U20). */
+/* Number of vocab slices S_v of the fixed split for a given vocab (numerics contract, U20):
+ * min(64, ceil(vocab / 256)) contiguous runs of whole 256-column tiles (64 at V = 151936).  The
+ * slice count fixes the merge order, so it depends on the vocabulary only; 64 slices let a
+ * small batch (one M-tile) spread over 64 CTA pairs. */
 int32_t tim_logprob_vocab_slices(int32_t vocab);
 
 /* ----------------------------------------------------------------------------

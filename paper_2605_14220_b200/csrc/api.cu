@@ -114,7 +114,10 @@ double i128_host_to_double(const int64_t* v) {
   return neg ? -r : r;
 }
 
-constexpr int kMaxSlices = 8;
+#ifndef TIM_MAX_SLICES
+#define TIM_MAX_SLICES 64
+#endif
+constexpr int kMaxSlices = TIM_MAX_SLICES;
 inline int32_t n_vocab_tiles(int32_t vocab) { return (vocab + 255) / 256; }
 inline int32_t vocab_slices(int32_t vocab) {
   const int32_t nvt = n_vocab_tiles(vocab);

@@ -45,10 +45,10 @@ def test_version_and_strings(L):
 
 
 def test_workspace_sizes(L):
-    assert L.tim_logprob_vocab_slices(151936) == 8
+    assert L.tim_logprob_vocab_slices(151936) == 64   # 594 tiles of 256 -> 64 slices of 9-10 tiles
     assert L.tim_logprob_vocab_slices(1024) == 4      # 4 tiles of 256 -> 4 slices
     assert L.tim_logprob_vocab_slices(1) == 1
-    assert L.tim_logprob_workspace_bytes(1000, 2048, 151936) == 1024 + 8 * 1000 * 16
+    assert L.tim_logprob_workspace_bytes(1000, 2048, 151936) == 1024 + 64 * 1000 * 16
     assert L.tim_correct_partial_bytes(5) == 128 + 5 * 32
     assert L.tim_correct_workspace_bytes(100, 5, 1) == 512 * 2
     assert L.tim_correct_workspace_bytes(100, 5, 4) == 512 * 5
@@ -93,7 +93,7 @@ def test_head_backward_argument_errors_are_synchronous(L):
     nb = (1 << 32) // (2 * 151936) // 256 * 256
     assert nb == 14080
     assert L.tim_head_backward_workspace_bytes(100000, 2048, 151936) == \
-        (1024 + 8 * nb * 16) + 3 * nb * 4 + nb * 151936 * 2
+        (1024 + 64 * nb * 16) + 3 * nb * 4 + nb * 151936 * 2
     assert L.tim_head_backward_workspace_bytes(1, 2048, 1000) == (1024 + 4 * 256 * 16) + 3 * 1024 + 256 * 1000 * 2
 
 
