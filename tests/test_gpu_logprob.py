@@ -203,6 +203,31 @@ def test_full_c1_batch_sampled_parity_and_invariance(tim):
     assert torch.isfinite(lp).all() and torch.isfinite(ent).all()
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_full_c2_c3_batches_sampled_parity_and_invariance(tim, name):
+    """C2 (256 x 8192 tokens, d = 4096) and C3 (512 x 16384 tokens, d = 2048) at full size, one
+    call as bench.py --config times it: 128 sampled rows vs the fp64 oracle, 16 of them re-scored
+    alone (bitwise), and a 256-row block re-scored as its own batch (bitwise)."""
+    cfg = synth.CONFIGS[name]
+    W = synth.head_weight(cfg.vocab, cfg.hidden, cfg.seed, device=DEV)
+    ids = synth.token_ids(cfg.n_tok, cfg.vocab, cfg.seed, device=DEV)
+    H = synth.hidden_states(cfg.n_tok, cfg.hidden, cfg.seed, device=DEV, weight=W, ids=ids, mode="peaked")
+    lp, ent = tim.logprob(H, W, ids)
+    rows = torch.randperm(cfg.n_tok, generator=torch.Generator().manual_seed(2))[:128].sort().values
+    rows_d = rows.to(DEV)
+    olp, oent = logprob_entropy(H[rows_d].cpu(), W.cpu(), ids[rows_d].cpu(), row_chunk=32)
+    assert np.abs(lp[rows_d].cpu().double().numpy() - olp).max() <= TOL
+    assert np.abs(ent[rows_d].cpu().double().numpy() - oent).max() <= TOL
+    for r in rows[:16].tolist():
+        a, b = tim.logprob(H[r:r + 1], W, ids[r:r + 1])
+        assert _bits(a)[0] == _bits(lp)[r] and _bits(b)[0] == _bits(ent)[r]
+    r0 = cfg.n_tok - 1000
+    a, b = tim.logprob(H[r0:r0 + 256], W, ids[r0:r0 + 256])
+    assert torch.equal(_bits(a), _bits(lp[r0:r0 + 256])) and torch.equal(_bits(b), _bits(ent[r0:r0 + 256]))
+    assert torch.isfinite(lp).all() and torch.isfinite(ent).all()
+
+
 @pytest.mark.parametrize("N,d,V", [(300, 256, 1000), (1, 64, 300), (2048, 2048, 151936), (1100, 512, 5000)])
 def test_multicast_cluster_variant_is_bitwise_identical(tim, N, d, V):
     """Clusters of two CTA pairs sharing W through TMA multicast (performance variant) must give
