@@ -299,6 +299,7 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
   constexpr bool kSeq = kSeqK != TIM_SEQ_NONE;  // kSeqK: the sequence score (TIM_SEQ_K1 / TIM_SEQ_K3)
   __shared__ LaneState sh_state[kLocalThreads];
   __shared__ __align__(128) float ring[kLocalWarps][kStages][2][kWarpTok];
+  __shared__ __align__(128) uint32_t ring_resp[kLocalWarps][kStages][kWarpTok / 4];
   __shared__ __align__(8) uint64_t ring_bar[kLocalWarps][kStages];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -351,17 +352,21 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
     fence_mbar_init();
   }
   __syncwarp();
+  // the response mask rides in the ring too when its address allows bulk copies (16-B aligned)
+  const bool resp_bulk = p.resp != nullptr && (reinterpret_cast<uintptr_t>(p.resp) & 15u) == 0;
+  const uint32_t resp0 = smem_u32(&ring_resp[wib][0][0]);
   auto issue = [&](int j, long long c) {  // lane 0: chunk c into stage j
     const uint32_t dst = ring0 + j * (2 * kWarpTok * 4);
-    mbar_arrive_expect_tx(bar0 + 8 * j, 2 * kWarpTok * 4);
+    mbar_arrive_expect_tx(bar0 + 8 * j, 2 * kWarpTok * 4 + (resp_bulk ? kWarpTok : 0));
     bulk_g2s(dst, p.num + c * kWarpTok, kWarpTok * 4, bar0 + 8 * j, pol);
     bulk_g2s(dst + kWarpTok * 4, p.den + c * kWarpTok, kWarpTok * 4, bar0 + 8 * j, pol);
+    if (resp_bulk) bulk_g2s(resp0 + j * kWarpTok, p.resp + c * kWarpTok, kWarpTok, bar0 + 8 * j, pol);
   };
   if (lane == 0)
     for (int j = 0; j < kStages; ++j)
       if (c_begin + j < c_mid) issue(j, c_begin + j);
   uint32_t r_nxt = 0x01010101u;
-  if (c_begin < c_mid && p.resp)
+  if (c_begin < c_mid && p.resp && !resp_bulk)
     r_nxt = __ldcs(reinterpret_cast<const unsigned int*>(p.resp + c_begin * kWarpTok + lane * kTpl));
   int cnt = 0, j = 0;
   uint32_t phase = 0;
@@ -370,8 +375,13 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
     mbar_wait(bar0 + 8 * j, phase);
     const float4 numv = *reinterpret_cast<const float4*>(&ring[wib][j][0][lane * kTpl]);
     const float4 denv = *reinterpret_cast<const float4*>(&ring[wib][j][1][lane * kTpl]);
-    const uint32_t resp = r_nxt;
-    if (c + 1 < c_mid && p.resp) r_nxt = __ldcs(reinterpret_cast<const unsigned int*>(p.resp + i0 + kWarpTok));
+    uint32_t resp;
+    if (resp_bulk) {
+      resp = ring_resp[wib][j][lane];
+    } else {
+      resp = r_nxt;
+      if (c + 1 < c_mid && p.resp) r_nxt = __ldcs(reinterpret_cast<const unsigned int*>(p.resp + i0 + kWarpTok));
+    }
     double dv[kTpl];
     dv[0] = __dsub_rn(static_cast<double>(numv.x), static_cast<double>(denv.x));
     dv[1] = __dsub_rn(static_cast<double>(numv.y), static_cast<double>(denv.y));
