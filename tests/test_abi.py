@@ -159,3 +159,15 @@ def test_tp_vocab_ranges_partition_the_vocabulary():
             assert rs[0][0] == 0 and rs[-1][1] == V
             for (a, b), (c, d) in zip(rs[:-1], rs[1:]):
                 assert b == c and a % 256 == 0 and a < b
+
+
+def test_missing_library_fails_loudly():
+    """No CPU fallback: without the built library every entry point raises (checked in a fresh
+    interpreter whose TIM_LIBRARY points nowhere)."""
+    import subprocess
+    import sys
+    code = ("from paper_2605_14220_b200 import tim\n"
+            "try:\n    tim.lib()\nexcept RuntimeError as e:\n    print('raised', 'not built' in str(e))\n")
+    env = dict(os.environ, TIM_LIBRARY=os.path.join(ROOT, "no_such_libtim.so"))
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+    assert "raised True" in r.stdout, r.stdout + r.stderr
