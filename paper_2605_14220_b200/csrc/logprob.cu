@@ -111,14 +111,26 @@ __device__ __forceinline__ uint64_t make_policy(int kind) {
 // ---------------------------------------------------------------- sampling twin (NEXT-1) --
 // Counter-based Philox4x32-10 (Salmon et al., SC'11): multipliers 0xD2511F53 / 0xCD9E8D57,
 // Weyl key increments 0x9E3779B9 / 0xBB67AE85.
-__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+// The key schedule (k0 + r W0, k1 + r W1) is the same for every block of the kernel: it is
+// expanded once (PhiloxKeys, warp-uniform) instead of per call.
+struct PhiloxKeys {
+  uint32_t k0[10], k1[10];
+  __device__ __forceinline__ PhiloxKeys(uint32_t a, uint32_t b) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+      k0[r] = a;
+      k1[r] = b;
+      a += 0x9E3779B9u;
+      b += 0xBB67AE85u;
+    }
+  }
+};
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, const PhiloxKeys& k) {
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
     const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
     const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
-    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
-    k0 += 0x9E3779B9u;
-    k1 += 0xBB67AE85u;
+    c = make_uint4(hi1 ^ c.y ^ k.k0[r], lo1, hi0 ^ c.w ^ k.k1[r], lo0);
   }
   return c;
 }
@@ -134,17 +146,19 @@ __device__ __forceinline__ float lg2_approx(float x) {
 // token's log-prob is bit-identical to tim_logprob's.  Strict '>' in ascending column order:
 // ties go to the lowest column.
 template <bool kTail>
-__device__ __forceinline__ void gumbel_chunk(const uint32_t (&r)[32], float c, int col0, int vocab, uint32_t sk0,
-                                             uint32_t sk1, uint32_t rk_lo, uint32_t rk_hi, float& best_s,
+__device__ __forceinline__ void gumbel_chunk(const uint32_t (&r)[32], float c, int col0, int vocab,
+                                             const PhiloxKeys& keys, uint32_t rk_lo, uint32_t rk_hi, float& best_s,
                                              float& best_y, int& best_col) {
 #pragma unroll
   for (int g = 0; g < 8; ++g) {
-    const uint4 x = philox4x32_10(make_uint4(static_cast<uint32_t>(col0 >> 2) + g, 0u, rk_lo, rk_hi), sk0, sk1);
+    const uint4 x = philox4x32_10(make_uint4(static_cast<uint32_t>(col0 >> 2) + g, 0u, rk_lo, rk_hi), keys);
     const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int i = 4 * g + q;
-      const float u = fmaf(static_cast<float>(xs[q] >> 9), 0x1p-23f, 0x1p-24f);
+      // u = ((x >> 9) + 1/2) 2^-23 exactly: 1.f with the 23 mantissa bits (x >> 9), minus
+      // (1 - 2^-24) (Sterbenz: exact) -- no int->float conversion on the XU pipe
+      const float u = __uint_as_float(0x3f800000u | (xs[q] >> 9)) - 0x1.fffffep-1f;
       const float y = __uint_as_float(r[i]) * c;
       float sc = y - lg2_approx(-lg2_approx(u));
       if (kTail && col0 + i >= vocab) sc = -CUDART_INF_F;
@@ -482,11 +496,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           else
             epi_chunk<false>(r, c, col0, p.vocab, a, m, s, uu, ya);
           if (kSample) {
-            const uint32_t sk0 = static_cast<uint32_t>(p.seed), sk1 = static_cast<uint32_t>(p.seed >> 32);
+            const PhiloxKeys keys(static_cast<uint32_t>(p.seed), static_cast<uint32_t>(p.seed >> 32));
             if (tail_tile)
-              gumbel_chunk<true>(r, c, col0, p.vocab, sk0, sk1, rk_lo, rk_hi, best_s, best_y, best_col);
+              gumbel_chunk<true>(r, c, col0, p.vocab, keys, rk_lo, rk_hi, best_s, best_y, best_col);
             else
-              gumbel_chunk<false>(r, c, col0, p.vocab, sk0, sk1, rk_lo, rk_hi, best_s, best_y, best_col);
+              gumbel_chunk<false>(r, c, col0, p.vocab, keys, rk_lo, rk_hi, best_s, best_y, best_col);
           }
         }
         acc ^= 1;
