@@ -219,6 +219,7 @@ def logprob(hidden: torch.Tensor, weight: torch.Tensor, ids: torch.Tensor, tempe
 
 
 _HOST_CHUNK = 65536          # rows per host->device chunk (a multiple of the 256-row pair tile)
+_HOST_FIRST = 8192           # the first chunks ramp up 8k, 16k, 32k: only a small copy is exposed
 _copy_streams: dict = {}
 
 
@@ -237,7 +238,11 @@ def _logprob_from_host(hidden, weight, ids, temperature, temperatures, entropy, 
     hd = torch.empty(N, d, dtype=torch.bfloat16, device=dev)
     ids_d = ids.to(dev, non_blocking=True).to(torch.int64)
     temps_d = temperatures.to(dev, non_blocking=True) if temperatures is not None else None
-    cuts = list(range(0, N, _HOST_CHUNK)) + [N]
+    cuts, a, step = [0], 0, _HOST_FIRST
+    while a < N:
+        a = min(N, a + step)
+        cuts.append(a)
+        step = min(2 * step, _HOST_CHUNK)
     evs = []
     cs.wait_stream(comp)
     with torch.cuda.stream(cs):
