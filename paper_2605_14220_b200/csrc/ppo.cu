@@ -20,8 +20,14 @@ namespace tim {
 
 constexpr int kPpoTpl = 4;                  // tokens per lane: one float4 of each input
 constexpr int kPpoWarpTok = 32 * kPpoTpl;
-constexpr int kPpoThreads = 256;
-constexpr int kPpoMinB = 2;
+#ifndef TIM_PPO_THREADS
+#define TIM_PPO_THREADS 256
+#endif
+#ifndef TIM_PPO_MINB
+#define TIM_PPO_MINB 2
+#endif
+constexpr int kPpoThreads = TIM_PPO_THREADS;
+constexpr int kPpoMinB = TIM_PPO_MINB;
 constexpr int kMaxHistBins = 1024;
 constexpr double kPpoFastLoss = 256.0;      // fast path: |loss| <= 2^8, so |X| <= 2^60 and four fit int64
 
@@ -132,13 +138,11 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
 
     float l_out[kPpoTpl], g_out[kPpoTpl];
     uint32_t cbits = 0;
-    long long cl = 0, ck1 = 0, ck3 = 0;  // chunk sums: |X| <= 2^60 (loss), 2^52 (K1, K3)
-    unsigned cn = 0, ccl = 0, cz = 0;
+    double loss_[kPpoTpl], r_[kPpoTpl];
 #pragma unroll
     for (int k = 0; k < kPpoTpl; ++k) {
       const double d = df[k];
-      const double k3 = k3f[k];
-      const double r = exp_from_k3_small(d, k3);
+      const double r = exp_from_k3_small(d, k3f[k]);
       const double A = static_cast<double>(ad_[k]);
       const bool clipped = (A > 0.0 && r > p.clip_hi) || (A < 0.0 && r < p.clip_lo);
       const double sv = clipped ? __dmul_rn(A > 0.0 ? p.clip_hi : p.clip_lo, A) : __dmul_rn(r, A);
@@ -148,17 +152,42 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
       l_out[k] = lf;
       g_out[k] = clipped ? 0.f : lf;
       cbits |= static_cast<uint32_t>(clipped) << (8 * k);
-      const bool use = wv_[k] != 0.f && !((slow >> k) & 1u);
-      const double lz = use ? loss : 0.0;
-      const double dz = use ? d : 0.0;
-      const double kz = use ? k3 : 0.0;
-      cl += __double2ll_rn(__dmul_rn(lz, kTwo52));
-      ck1 += __double2ll_rn(__dmul_rn(-dz, kTwo52));
-      ck3 += __double2ll_rn(__dmul_rn(kz, kTwo52));
-      cn += use ? 1u : 0u;
-      ccl += (use && clipped) ? 1u : 0u;
-      cz += (use && A == 0.0) ? 1u : 0u;
-      if (use && A != 0.0) atomicAdd(&sh_hist[(A > 0.0 ? 0 : nslot) + hist_slot(p, r, A)], 1);
+      loss_[k] = loss;
+      r_[k] = r;
+    }
+    long long cl = 0, ck1 = 0, ck3 = 0;  // chunk sums: |X| <= 2^60 (loss), 2^52 (K1, K3)
+    unsigned cn = 0, ccl = 0, cz = 0;
+    // warp-uniform: every token of the chunk fast and weighted (the common case inside the
+    // response) -> the sums without per-token masks
+    const bool lane_clean = slow == 0u && wv_[0] != 0.f && wv_[1] != 0.f && wv_[2] != 0.f && wv_[3] != 0.f;
+    if (__all_sync(0xffffffffu, lane_clean)) {
+#pragma unroll
+      for (int k = 0; k < kPpoTpl; ++k) {
+        const double A = static_cast<double>(ad_[k]);
+        cl += __double2ll_rn(__dmul_rn(loss_[k], kTwo52));
+        ck1 += __double2ll_rn(__dmul_rn(-df[k], kTwo52));
+        ck3 += __double2ll_rn(__dmul_rn(k3f[k], kTwo52));
+        ccl += (cbits >> (8 * k)) & 1u;
+        if (A == 0.0) cz += 1u;
+        else atomicAdd(&sh_hist[(A > 0.0 ? 0 : nslot) + hist_slot(p, r_[k], A)], 1);
+      }
+      cn = kPpoTpl;
+    } else {
+#pragma unroll
+      for (int k = 0; k < kPpoTpl; ++k) {
+        const double A = static_cast<double>(ad_[k]);
+        const bool use = wv_[k] != 0.f && !((slow >> k) & 1u);
+        const double lz = use ? loss_[k] : 0.0;
+        const double dz = use ? df[k] : 0.0;
+        const double kz = use ? k3f[k] : 0.0;
+        cl += __double2ll_rn(__dmul_rn(lz, kTwo52));
+        ck1 += __double2ll_rn(__dmul_rn(-dz, kTwo52));
+        ck3 += __double2ll_rn(__dmul_rn(kz, kTwo52));
+        cn += use ? 1u : 0u;
+        ccl += (use && ((cbits >> (8 * k)) & 1u)) ? 1u : 0u;
+        cz += (use && A == 0.0) ? 1u : 0u;
+        if (use && A != 0.0) atomicAdd(&sh_hist[(A > 0.0 ? 0 : nslot) + hist_slot(p, r_[k], A)], 1);
+      }
     }
     s_loss += cl;
     acc.x += cl;
