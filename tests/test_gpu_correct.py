@@ -188,3 +188,25 @@ def test_nccl_comm_path_single_rank(tim):
     finally:
         if own:
             dist.destroy_process_group()
+
+
+def test_alignment_variants_match_the_oracle(tim):
+    """The pass-1 load paths: 16-B aligned log-probs with a 16-B aligned mask (everything through
+    the bulk-copy ring), with a mask that is only 4-B aligned (register prefetch of the mask), and
+    4-B aligned log-probs (element-wise path) -- all bit-exact vs the oracle."""
+    num, den, cu, mask = _inputs(24, 2000, 77)
+    N = int(cu[-1])
+    c = tim.CorrectConfig(tis=True, tok_rs=True, tok_lo=0.8, tok_hi=1.25, seq_rs=oc.SEQ_K3,
+                          seq_agg=oc.AGG_MEAN, tau_seq=1e-3)
+    pad = 8
+    for off_lp, off_m in ((0, 0), (0, 4), (4, 4), (1, 3)):
+        nb = torch.zeros(N + pad, dtype=torch.float32)
+        db = torch.zeros(N + pad, dtype=torch.float32)
+        mb = torch.zeros(N + pad, dtype=torch.uint8)
+        nb[off_lp:off_lp + N] = num
+        db[off_lp:off_lp + N] = den
+        mb[off_m:off_m + N] = mask
+        nd, dd, md = nb.to(DEV), db.to(DEV), mb.to(DEV)
+        res = tim.correct(nd[off_lp:off_lp + N], dd[off_lp:off_lp + N], cu.to(DEV), c, md[off_m:off_m + N])
+        ref = oc.correct(num.numpy(), den.numpy(), cu.numpy(), _ocfg(c), mask.numpy())
+        _compare(res, ref, c)
