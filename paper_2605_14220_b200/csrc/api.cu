@@ -94,6 +94,19 @@ bool encode_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t co
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// G block [rows][pitch] bf16 as the gradient epilogue's TMA store target: 32 x 32 tiles, 64-B swizzle
+bool encode_g_store(CUtensorMap* m, void* base, uint64_t rows, uint64_t cols, uint64_t pitch_elems) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch_elems * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 
 // int128 {lo, hi} -> double, round to nearest even (bits below 64 significant ones fold into a sticky bit)
@@ -858,7 +871,9 @@ tim_status tim_head_backward(const void* hidden_bf16, int64_t ld_hidden, const v
     if (g_max_clusters > 0 && g_max_clusters < cap) cap = g_max_clusters;
     const int64_t groups = n_units < cap ? n_units : cap;
     p.group = pick_group(dev, true, S, groups, d);
-    if (launch_head_grad(th, tw, p, static_cast<int>(groups * 2), s) != cudaSuccess) return TIM_ERR_CUDA;
+    CUtensorMap tg;
+    if (!encode_g_store(&tg, G, nbc, vocab, g_ld)) return TIM_ERR_CUDA;
+    if (launch_head_grad(th, tw, tg, p, static_cast<int>(groups * 2), s) != cudaSuccess) return TIM_ERR_CUDA;
     // (3) dH[b] = G W  (column-major: dH^T[d x nbc] = W^T[d x V] G^T[V x nbc])
     if (dhidden_or_null) {
       st = gemm_bf16_f32(s, kCublasOpN, kCublasOpN, d, static_cast<int>(nbc), vocab, weight_bf16, d, G,

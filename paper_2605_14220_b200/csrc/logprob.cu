@@ -240,11 +240,13 @@ __device__ __noinline__ uint32_t wait_progress(const uint32_t* prog, uint32_t nc
 // M-tiles, sweep the same vocab tiles in lock-step and share every W tile through TMA multicast).
 // ------------------------------------------------------------ head backward (NEXT-3) --
 // G[t, v] = dL/dz[t, v] = (1/T) [ g (1[v = a] - p) - e p (ln p + H) ] for L = sum_t g_t logp_t +
-// e_t H_t, with p = 2^(y - lse2) from the forward's log2-sum-exp; written as bf16 to the slice's
-// G block (row-major, ld = p.g_ld) for the two library GEMMs dH = G W and dW = G^T H.
+// e_t H_t, with p = 2^(y - lse2) from the forward's log2-sum-exp; written as bf16 to the G block
+// (row-major, ld = p.g_ld) for the two library GEMMs dH = G W and dW = G^T H: each warp stages
+// its 32 rows x 32 columns in shared memory and one lane writes the tile with a TMA store
+// (tmap_g), instead of 32 scattered 64-B row segments per chunk.
 __device__ __forceinline__ void grad_chunk(const uint32_t (&r)[32], float c, int col0, int vocab, int64_t a,
-                                           float gl, float ge, float gH, float lse2, float invT,
-                                           const LogprobParams& p, int row) {
+                                           float gl, float ge, float gH, float lse2, float invT, uint32_t stage,
+                                           int lane) {
   constexpr float kLn2 = 0.69314718055994530942f;
   uint32_t packed[16];
 #pragma unroll
@@ -261,23 +263,22 @@ __device__ __forceinline__ void grad_chunk(const uint32_t (&r)[32], float c, int
     const __nv_bfloat162 b = __floats2bfloat162_rn(gv[0], gv[1]);
     packed[i / 2] = *reinterpret_cast<const uint32_t*>(&b);
   }
-  const int lc0 = col0 - p.g_col0;  // column inside this slice's G block
-  uint16_t* dst = p.g_out + static_cast<int64_t>(row) * p.g_ld + lc0;
-  if (col0 + 32 <= vocab) {
-    uint4* d4 = reinterpret_cast<uint4*>(dst);
+  (void)vocab;
+  // this row's 64 B into the warp's 32 x 32 bf16 staging tile, 16-B chunks swizzled as the
+  // tensor map's SWIZZLE_64B expects (chunk ^ ((row >> 1) & 3)): conflict-free shared stores
 #pragma unroll
-    for (int v = 0; v < 4; ++v)
-      d4[v] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
-  } else {
-    for (int i = 0; i < 32 && col0 + i < vocab; ++i)
-      dst[i] = static_cast<uint16_t>(packed[i / 2] >> (16 * (i & 1)));
+  for (int v = 0; v < 4; ++v) {
+    const uint32_t addr = stage + lane * 64 + ((v ^ ((lane >> 1) & 3)) << 4);
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(packed[4 * v]), "r"(packed[4 * v + 1]),
+                 "r"(packed[4 * v + 2]), "r"(packed[4 * v + 3])
+                 : "memory");
   }
 }
 
 template <bool kPair, bool kDebug, bool kSample, int kNP, bool kGrad = false>
 __global__ void __launch_bounds__(kThreads, 1)
     logprob_fwd_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constant__ CUtensorMap tmap_w,
-                       LogprobParams p) {
+                       const __grid_constant__ CUtensorMap tmap_g, LogprobParams p) {
   using C = KCfg<kPair>;
   static_assert(kNP == 1 || (kPair && kNP == 2), "multicast clusters are built from CTA pairs");
   extern __shared__ uint8_t smem_raw[];
@@ -440,6 +441,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row_in_cta = q * 32 + lane;
     const uint32_t tempty_leader = kPair ? mapa(smem_u32(tempty), pl) : smem_u32(tempty);
     uint32_t acc = 0, aphase = 0;
+    // gradient mode: two 2-KB staging tiles per epilogue warp (1024-B aligned for the swizzle)
+    const uint32_t gstage0 =
+        kGrad ? ((smem_u32(smem + C::kStages * C::kStageBytes + 256) + 1023u) & ~1023u) + (warp - 2) * 4096u : 0u;
+    int gbuf = 0;
     int dm, j;
     for (int k = 0; sched.unit(cid, k, dm, j); ++k) {
       const int mt = dm * kNP + pid;
@@ -490,7 +495,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (col0 + i < p.vocab) dst[i] = __uint_as_float(r[i]);
           }
           if (kGrad) {
-            if (valid) grad_chunk(r, c, col0, p.vocab, a, gl, ge, gH, lse2, invT, p, row);
+            const uint32_t stage = gstage0 + gbuf * 2048u;
+            if (lane == 0) bulk_wait_group_read<1>();  // this buffer's previous store has read it
+            __syncwarp();
+            grad_chunk(r, c, col0, p.vocab, a, gl, ge, gH, lse2, invT, stage, lane);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmap_g, stage, col0 - p.g_col0, row - lane);
+              bulk_commit_group();
+            }
+            gbuf ^= 1;
           } else if (tail_tile)
             epi_chunk<true>(r, c, col0, p.vocab, a, m, s, uu, ya);
           else
@@ -515,6 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
+  if (kGrad && warp >= 2 && lane == 0) bulk_wait_group_all();  // the G tiles are written
   __syncwarp();
   tc_fence_before();
   if (kPair) cluster_sync(); else __syncthreads();
@@ -598,19 +614,21 @@ __global__ void __launch_bounds__(256) sample_merge_kernel(MergeParams p) {
 
 template <bool kPair, bool kDebug, bool kSample, int kNP, bool kGrad = false>
 static cudaError_t launch_fwd(const CUtensorMap& th, const CUtensorMap& tw, const LogprobParams& p, int grid,
-                              cudaStream_t stream) {
+                              cudaStream_t stream, const CUtensorMap* tg = nullptr) {
   using C = KCfg<kPair>;
   auto kern = logprob_fwd_kernel<kPair, kDebug, kSample, kNP, kGrad>;
+  // gradient mode: + 1 KB alignment slack and 4 warps x 2 x 2 KB G staging tiles
+  constexpr int kSmem = C::kSmemBytes + (kGrad ? 1024 + kEpiWarps * 4096 : 0);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = C::kSmemBytes;
+  cfg.dynamicSmemBytes = kSmem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -619,15 +637,15 @@ static cudaError_t launch_fwd(const CUtensorMap& th, const CUtensorMap& tw, cons
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, th, tw, p);
+  return cudaLaunchKernelEx(&cfg, kern, th, tw, tg ? *tg : th, p);
 }
 
 int fwd_unit_rows(bool pair) { return pair ? KCfg<true>::kUnitM : KCfg<false>::kUnitM; }
 int fwd_w_box_rows(bool pair) { return pair ? KCfg<true>::kBRows : KCfg<false>::kBRows; }
 
-cudaError_t launch_head_grad(const CUtensorMap& th, const CUtensorMap& tw, const LogprobParams& p, int grid,
-                             cudaStream_t stream) {
-  return launch_fwd<true, false, false, 1, true>(th, tw, p, grid, stream);
+cudaError_t launch_head_grad(const CUtensorMap& th, const CUtensorMap& tw, const CUtensorMap& tg,
+                             const LogprobParams& p, int grid, cudaStream_t stream) {
+  return launch_fwd<true, false, false, 1, true>(th, tw, p, grid, stream, &tg);
 }
 
 cudaError_t launch_logprob_fwd(bool pair, bool debug, bool sample, bool quad, const CUtensorMap& th,
