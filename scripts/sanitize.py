@@ -19,8 +19,9 @@ mask = synth.resp_mask(cu.cpu(), 10).to(dev)
 roll = synth.perturb_laplace_mix(lp, 3)
 res = tim.correct(lp, roll, cu, tim.PRESETS["tis-srs-k3-corr-ratio"], mask)
 pp = tim.ppo_loss(lp, roll, torch.randn(300, device=dev), cu, tim.PPOConfig(), coeff=res["coeff"])
+dh, dw = tim.head_backward(H, W, ids, torch.ones(300, device=dev), torch.full((300,), 0.01, device=dev))
 torch.cuda.synchronize()
-print("sanitize run ok", float(lp.sum()), res["stats"]["n_seq_rejected"], pp["stats"]["n_clipped"])
+print("sanitize run ok", float(lp.sum()), res["stats"]["n_seq_rejected"], pp["stats"]["n_clipped"], float(dh.abs().sum()))
 # a larger correction / PPO call: several chunks per warp, so the per-warp TMA ring of the
 # correction kernel wraps around (stages refilled), with variable-length sequences
 cu2 = synth.cu_seqlens(256, 16384, variable=True, seed=11).to(dev)
