@@ -99,6 +99,18 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def _ncu_tensor_pct(config: str):
+    """ncu tensor-pipe activity of the logprob kernel (committed --set full summary; C1 only)."""
+    if config != "c1":
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_logprob_summary.json")) as f:
+            m = json.load(f)["metrics"]
+        return float(m["sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"][0])
+    except Exception:
+        return None
+
+
 def _traffic(config: str):
     """dram bytes per launch of the logprob kernel on this config, from the committed ncu --set
     full summary (None when no capture of this config is committed)."""
@@ -367,6 +379,7 @@ def run_ours(args):
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "frac_of_burst": achieved / float(peaks["bf16_tflops"]),
                      "peak_source": peak_src + " bf16_tflops_sustained", "traffic": _traffic(cfg.name),
+                     "ncu_tensor_pipe_pct": _ncu_tensor_pct(cfg.name),
                      "kernel": "tim_logprob (tcgen05 GEMM + fused epilogue + slice merge)",
                      "kernel_ms": lp_ms, "algorithmic_flop_per_token": 2 * cfg.vocab * cfg.hidden},
         "clocks": clk,
