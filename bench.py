@@ -18,9 +18,16 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import sys
+
+# The reference arm (--impl reference) runs the CPU oracle on rank 0 alone: give its BLAS every
+# host core even when the launcher (torchrun) pinned OMP_NUM_THREADS=1 for the per-GPU ranks.
+# This has to happen before numpy / torch load OpenBLAS.
+if "--impl" in sys.argv and "reference" in sys.argv and os.environ.get("RANK", "0") == "0":
+    for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS"):
+        os.environ[_v] = str(os.cpu_count() or 1)
 import statistics
 import subprocess
-import sys
 import tempfile
 import threading
 import time
