@@ -403,11 +403,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (publish && lane == 0) st_relaxed_gpu(p.progress + cid, 0xFFFFFFFFu);
   } else if (warp == 1) {
-    // ===================== MMA issuer (one thread of the leader CTA) =====================
-    if (leader && lane == 0) {
+    // ===================== MMA issuer (the leader CTA's warp 1) =====================
+    // The whole warp runs the loop (warp-uniform waits and descriptors); one lane issues each
+    // tcgen05 instruction (elect.sync).  Shared-memory descriptors advance by constants: stage s
+    // and K-step kk of operand A start at a0 + s * kABytes + kk * 32 bytes, i.e. the descriptor's
+    // address field (bits 0-13, address >> 4) plus s * kABytes / 16 + 2 kk.
+    if (leader) {
       const uint32_t idesc = umma_idesc_bf16_f32(kPair ? 256 : 128, kTileN);
       const uint16_t mask_empty = kNP == 2 ? 0xF : (kPair ? 0x3 : 0x1);
       const uint16_t mask_full = static_cast<uint16_t>((kPair ? 0x3 : 0x1) << pl);
+      const uint64_t desc_a0 = umma_desc_sw128(smem_u32(smem_a));
+      const uint64_t desc_b0 = umma_desc_sw128(smem_u32(smem_b));
       uint32_t stage = 0, phase = 0, acc = 0, aphase = 0;
       int dm, j;
       for (int k = 0; sched.unit(cid, k, dm, j); ++k) {
@@ -419,17 +425,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kb = 0; kb < nkb; ++kb) {
             mbar_wait(smem_u32(&full[stage]), phase);
             tc_fence_after();
-            const uint32_t a0 = smem_u32(smem_a + stage * C::kABytes);
-            const uint32_t b0 = smem_u32(smem_b + stage * C::kBBytes);
+            const uint64_t da = desc_a0 + stage * (C::kABytes >> 4);
+            const uint64_t db = desc_b0 + stage * (C::kBBytes >> 4);
 #pragma unroll
-            for (int kk = 0; kk < kBlockK / kUmmaK; ++kk) {
-              umma_bf16<C::kCtaGroup>(d_tmem, umma_desc_sw128(a0 + kk * kUmmaK * 2),
-                                      umma_desc_sw128(b0 + kk * kUmmaK * 2), idesc, (kb | kk) != 0);
-            }
-            umma_commit_mc<C::kCtaGroup>(smem_u32(&empty[stage]), mask_empty);
+            for (int kk = 0; kk < kBlockK / kUmmaK; ++kk)
+              umma_bf16_elect<C::kCtaGroup>(d_tmem, da + 2 * kk, db + 2 * kk, idesc, (kb | kk) != 0);
+            umma_commit_mc_elect<C::kCtaGroup>(smem_u32(&empty[stage]), mask_empty);
             if (++stage == C::kStages) { stage = 0; phase ^= 1; }
           }
-          umma_commit_mc<C::kCtaGroup>(smem_u32(&tfull[acc]), mask_full);
+          umma_commit_mc_elect<C::kCtaGroup>(smem_u32(&tfull[acc]), mask_full);
           acc ^= 1;
           if (acc == 0) aphase ^= 1;
         }
