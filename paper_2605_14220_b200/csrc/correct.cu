@@ -355,16 +355,15 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
   // the response mask rides in the ring too when its address allows bulk copies (16-B aligned)
   const bool resp_bulk = p.resp != nullptr && (reinterpret_cast<uintptr_t>(p.resp) & 15u) == 0;
   const uint32_t resp0 = smem_u32(&ring_resp[wib][0][0]);
-  auto issue = [&](int j, long long c) {  // lane 0: chunk c into stage j
+  auto issue = [&](int j, long long c) {  // whole warp (one elected lane issues): chunk c into stage j
     const uint32_t dst = ring0 + j * (2 * kWarpTok * 4);
-    mbar_arrive_expect_tx(bar0 + 8 * j, 2 * kWarpTok * 4 + (resp_bulk ? kWarpTok : 0));
-    bulk_g2s(dst, p.num + c * kWarpTok, kWarpTok * 4, bar0 + 8 * j, pol);
-    bulk_g2s(dst + kWarpTok * 4, p.den + c * kWarpTok, kWarpTok * 4, bar0 + 8 * j, pol);
-    if (resp_bulk) bulk_g2s(resp0 + j * kWarpTok, p.resp + c * kWarpTok, kWarpTok, bar0 + 8 * j, pol);
+    mbar_arrive_expect_tx_elect(bar0 + 8 * j, 2 * kWarpTok * 4 + (resp_bulk ? kWarpTok : 0));
+    bulk_g2s_elect(dst, p.num + c * kWarpTok, kWarpTok * 4, bar0 + 8 * j, pol);
+    bulk_g2s_elect(dst + kWarpTok * 4, p.den + c * kWarpTok, kWarpTok * 4, bar0 + 8 * j, pol);
+    if (resp_bulk) bulk_g2s_elect(resp0 + j * kWarpTok, p.resp + c * kWarpTok, kWarpTok, bar0 + 8 * j, pol);
   };
-  if (lane == 0)
-    for (int j = 0; j < kStages; ++j)
-      if (c_begin + j < c_mid) issue(j, c_begin + j);
+  for (int j = 0; j < kStages; ++j)
+    if (c_begin + j < c_mid) issue(j, c_begin + j);
   uint32_t r_nxt = 0x01010101u;
   if (c_begin < c_mid && p.resp && !resp_bulk)
     r_nxt = __ldcs(reinterpret_cast<const unsigned int*>(p.resp + c_begin * kWarpTok + lane * kTpl));
@@ -387,11 +386,9 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
     dv[1] = __dsub_rn(static_cast<double>(numv.y), static_cast<double>(denv.y));
     dv[2] = __dsub_rn(static_cast<double>(numv.z), static_cast<double>(denv.z));
     dv[3] = __dsub_rn(static_cast<double>(numv.w), static_cast<double>(denv.w));
-    __syncwarp();  // every lane has read stage j: refill it with chunk c + kStages
-    if (lane == 0 && c + kStages < c_mid) {
-      fence_proxy_async_smem();
-      issue(j, c + kStages);
-    }
+    fence_proxy_async_smem();  // this lane's reads of stage j before the async refill
+    __syncwarp();              // every lane has read stage j: refill it with chunk c + kStages
+    if (c + kStages < c_mid) issue(j, c + kStages);
     if (++j == kStages) {
       j = 0;
       phase ^= 1u;
