@@ -354,7 +354,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < nkb; ++kb) {
           if (p.sleep_waits) mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
           else mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
-          if (lane == 0) {
+          if (kPair && kNP == 1 && hints) {
+            // the default path, warp-wide: one elected lane issues (no single-lane issue loops)
+            const uint32_t fb_local = smem_u32(&full[stage]);
+            if (leader) mbar_arrive_expect_tx_elect(fb_local, 2 * C::kStageBytes);
+            const uint32_t fb = mapa(fb_local, 0);
+            tma_load_2d_pair_hint_elect(smem_u32(smem_a + stage * C::kABytes), &tmap_h, fb, kb * kBlockK, m0, pol_h);
+            tma_load_2d_pair_hint_elect(smem_u32(smem_b + stage * C::kBBytes), &tmap_w, fb, kb * kBlockK, n0, pol_w);
+          } else if (lane == 0) {
             const uint32_t fb_local = smem_u32(&full[stage]);
             const uint32_t a_dst = smem_u32(smem_a + stage * C::kABytes);
             const uint32_t b_dst = smem_u32(smem_b + stage * C::kBBytes);

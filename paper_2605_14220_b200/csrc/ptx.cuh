@@ -144,6 +144,16 @@ __device__ __forceinline__ void tma_load_2d_pair_hint(uint32_t smem_dst, const v
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(cluster_bar), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
+// warp-wide form (converged warp, identical operands): one elected lane issues
+__device__ __forceinline__ void tma_load_2d_pair_hint_elect(uint32_t smem_dst, const void* tmap, uint32_t cluster_bar,
+                                                            int32_t c0, int32_t c1, uint64_t policy) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;\n\t}" ::"r"(smem_dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(cluster_bar), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
 // 2-D tile load issued by one CTA of a CTA pair and multicast to the CTAs in `cta_mask` (same
 // shared-memory offset in each); `pair_bar` is the local barrier address with the peer bit cleared,
 // so each destination's bytes are counted on the leader barrier of the destination's own pair.
