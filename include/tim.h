@@ -345,6 +345,35 @@ tim_status tim_head_backward(const void* hidden_bf16, int64_t ld_hidden, const v
                              tim_device_status* dstatus, void* stream);
 
 /* ----------------------------------------------------------------------------
+ * tim_logprob_saved / tim_head_backward_saved  (NEXT-3 for a trainer that keeps forward state:
+ * the backward then skips its own forward pass -- 3 instead of 4 passes over the logits)
+ *
+ * tim_logprob_saved = tim_logprob (same arguments, outputs, errors and numerics) that also
+ *   writes lse2_out[t] = log2 sum_v 2^(y[t,v]), y = z log2(e) / T_t (fp32, the value the merge
+ *   forms in fp64 then rounds); entropy_out and lse2_out are required ([n_tok] fp32 each).
+ * tim_head_backward_saved = tim_head_backward given the forward's entropy_saved / lse2_saved
+ *   (from tim_logprob_saved on the SAME hidden, weight, ids and temperatures -- they are not
+ *   re-validated here; bad ids / temperatures were reported by that forward call).  Because the
+ *   forward is batch-invariant, the outputs are bitwise those of tim_head_backward on the same
+ *   inputs.  Same workspace size and the other arguments / errors as tim_head_backward;
+ *   entropy_saved / lse2_saved NULL -> TIM_ERR_NULL (n_tok > 0).
+ * -------------------------------------------------------------------------- */
+tim_status tim_logprob_saved(const void* hidden_bf16, int64_t ld_hidden, const void* weight_bf16,
+                             int32_t hidden, int32_t vocab, const int64_t* token_ids, int64_t n_tok,
+                             float temperature, const float* temperatures_or_null,
+                             float* logp_out, float* entropy_out, float* lse2_out,
+                             void* workspace, size_t workspace_bytes,
+                             tim_device_status* dstatus, void* stream);
+tim_status tim_head_backward_saved(const void* hidden_bf16, int64_t ld_hidden, const void* weight_bf16,
+                                   int32_t hidden, int32_t vocab, const int64_t* token_ids, int64_t n_tok,
+                                   float temperature, const float* temperatures_or_null,
+                                   const float* entropy_saved, const float* lse2_saved,
+                                   const float* grad_logp, const float* grad_ent_or_null,
+                                   float* dhidden_or_null, float* dweight_or_null,
+                                   void* workspace, size_t workspace_bytes,
+                                   tim_device_status* dstatus, void* stream);
+
+/* ----------------------------------------------------------------------------
  * tim_ppo_loss  (fused PPO / GRPO surrogate + loss diagnostics)
  *
  * Per token t (PAPER.md eq:ppo_loss P:352-360, eq:ppo_ratio P:361-373, App. A.4):

@@ -782,11 +782,26 @@ size_t tim_head_backward_workspace_bytes(int64_t n_tok, int32_t hidden, int32_t 
          static_cast<size_t>(nb) * static_cast<size_t>(bwd_g_ld(vocab)) * 2u;
 }
 
-tim_status tim_head_backward(const void* hidden_bf16, int64_t ld_hidden, const void* weight_bf16, int32_t d,
+tim_status tim_logprob_saved(const void* hidden_bf16, int64_t ld_hidden, const void* weight_bf16, int32_t hidden,
                              int32_t vocab, const int64_t* token_ids, int64_t n_tok, float temperature,
-                             const float* temps, const float* grad_logp, const float* grad_ent_or_null,
-                             float* dhidden_or_null, float* dweight_or_null, void* ws, size_t ws_bytes,
-                             tim_device_status* dstatus, void* stream) {
+                             const float* temperatures_or_null, float* logp_out, float* entropy_out,
+                             float* lse2_out, void* workspace, size_t workspace_bytes, tim_device_status* dstatus,
+                             void* stream) {
+  if (n_tok > 0 && (!entropy_out || !lse2_out)) return TIM_ERR_NULL;
+  return logprob_impl(hidden_bf16, ld_hidden, weight_bf16, hidden, vocab, token_ids, n_tok, temperature,
+                      temperatures_or_null, logp_out, entropy_out, workspace, workspace_bytes, dstatus, stream,
+                      nullptr, 0, nullptr, 0, nullptr, 1, 0, nullptr, lse2_out, 0);
+}
+
+// ent_saved / lse2_saved null: run the forward per token block (tim_head_backward); else take the
+// forward's per-token entropy and log2-sum-exp from the caller (tim_head_backward_saved).
+static tim_status head_backward_impl(const void* hidden_bf16, int64_t ld_hidden, const void* weight_bf16, int32_t d,
+                                     int32_t vocab, const int64_t* token_ids, int64_t n_tok, float temperature,
+                                     const float* temps, const float* ent_saved, const float* lse2_saved,
+                                     const float* grad_logp, const float* grad_ent_or_null,
+                                     float* dhidden_or_null, float* dweight_or_null, void* ws, size_t ws_bytes,
+                                     tim_device_status* dstatus, void* stream) {
+  const bool saved = ent_saved != nullptr;
   if (!weight_bf16) return TIM_ERR_NULL;
   if (n_tok < 0 || n_tok >= (int64_t(1) << 31)) return TIM_ERR_SHAPE;
   if (d < 64 || d > 16384 || d % 64 != 0) return TIM_ERR_SHAPE;
@@ -804,6 +819,7 @@ tim_status tim_head_backward(const void* hidden_bf16, int64_t ld_hidden, const v
     return TIM_OK;
   }
   if (!hidden_bf16 || !token_ids || !grad_logp || !ws) return TIM_ERR_NULL;
+  if (saved && !lse2_saved) return TIM_ERR_NULL;
   if (!aligned(hidden_bf16, 16) || !aligned(ws, 256)) return TIM_ERR_ALIGN;
   if (dhidden_or_null && !aligned(dhidden_or_null, 16)) return TIM_ERR_ALIGN;
   if (ws_bytes < tim_head_backward_workspace_bytes(n_tok, d, vocab)) return TIM_ERR_WORKSPACE;
@@ -817,8 +833,8 @@ tim_status tim_head_backward(const void* hidden_bf16, int64_t ld_hidden, const v
   const size_t fwd_bytes = al256(tim_logprob_workspace_bytes(nb, d, vocab));
   uint8_t* fwd_ws = w8;
   float* logp = reinterpret_cast<float*>(w8 + fwd_bytes);
-  float* ent = reinterpret_cast<float*>(w8 + fwd_bytes + al256(nb * 4));
-  float* lse2 = reinterpret_cast<float*>(w8 + fwd_bytes + 2 * al256(nb * 4));
+  float* ent_ws = reinterpret_cast<float*>(w8 + fwd_bytes + al256(nb * 4));
+  float* lse2_ws = reinterpret_cast<float*>(w8 + fwd_bytes + 2 * al256(nb * 4));
   uint16_t* G = reinterpret_cast<uint16_t*>(w8 + fwd_bytes + 3 * al256(nb * 4));
   const int32_t S = vocab_slices(vocab);
   const int32_t nvt = n_vocab_tiles(vocab);
@@ -832,10 +848,16 @@ tim_status tim_head_backward(const void* hidden_bf16, int64_t ld_hidden, const v
     const int64_t nbc = (n_tok - b0 < nb) ? n_tok - b0 : nb;
     const void* hb = static_cast<const uint8_t*>(hidden_bf16) + b0 * ld_hidden * 2;
     const float* tb = temps ? temps + b0 : nullptr;
-    // (1) forward: logp, H, log2-sum-exp of the block (the same kernel and numerics as tim_logprob)
-    st = logprob_impl(hb, ld_hidden, weight_bf16, d, vocab, token_ids + b0, nbc, temperature, tb, logp, ent,
-                      fwd_ws, fwd_bytes, dstatus, stream, nullptr, 0, nullptr, 0, nullptr, 1, 0, nullptr, lse2, b0);
-    if (st != TIM_OK) return st;
+    // (1) forward: logp, H, log2-sum-exp of the block (the same kernel and numerics as tim_logprob),
+    //     unless the caller saved them (tim_logprob_saved; batch-invariant, so the same values)
+    const float* ent = saved ? ent_saved + b0 : ent_ws;
+    const float* lse2 = saved ? lse2_saved + b0 : lse2_ws;
+    if (!saved) {
+      st = logprob_impl(hb, ld_hidden, weight_bf16, d, vocab, token_ids + b0, nbc, temperature, tb, logp, ent_ws,
+                        fwd_ws, fwd_bytes, dstatus, stream, nullptr, 0, nullptr, 0, nullptr, 1, 0, nullptr, lse2_ws,
+                        b0);
+      if (st != TIM_OK) return st;
+    }
     // (2) recompute the logits tile by tile; the epilogue writes G = dL/dz (bf16) instead of LSE partials
     CUtensorMap th;
     if (!encode_bf16_2d(&th, hb, nbc, d, ld_hidden, 128)) return TIM_ERR_CUDA;
@@ -888,6 +910,28 @@ tim_status tim_head_backward(const void* hidden_bf16, int64_t ld_hidden, const v
     }
   }
   return TIM_OK;
+}
+
+tim_status tim_head_backward(const void* hidden_bf16, int64_t ld_hidden, const void* weight_bf16, int32_t d,
+                             int32_t vocab, const int64_t* token_ids, int64_t n_tok, float temperature,
+                             const float* temps, const float* grad_logp, const float* grad_ent_or_null,
+                             float* dhidden_or_null, float* dweight_or_null, void* ws, size_t ws_bytes,
+                             tim_device_status* dstatus, void* stream) {
+  return head_backward_impl(hidden_bf16, ld_hidden, weight_bf16, d, vocab, token_ids, n_tok, temperature, temps,
+                            nullptr, nullptr, grad_logp, grad_ent_or_null, dhidden_or_null, dweight_or_null, ws,
+                            ws_bytes, dstatus, stream);
+}
+
+tim_status tim_head_backward_saved(const void* hidden_bf16, int64_t ld_hidden, const void* weight_bf16, int32_t d,
+                                   int32_t vocab, const int64_t* token_ids, int64_t n_tok, float temperature,
+                                   const float* temps, const float* entropy_saved, const float* lse2_saved,
+                                   const float* grad_logp, const float* grad_ent_or_null, float* dhidden_or_null,
+                                   float* dweight_or_null, void* ws, size_t ws_bytes, tim_device_status* dstatus,
+                                   void* stream) {
+  if (n_tok > 0 && (!entropy_saved || !lse2_saved)) return TIM_ERR_NULL;
+  return head_backward_impl(hidden_bf16, ld_hidden, weight_bf16, d, vocab, token_ids, n_tok, temperature, temps,
+                            entropy_saved, lse2_saved, grad_logp, grad_ent_or_null, dhidden_or_null,
+                            dweight_or_null, ws, ws_bytes, dstatus, stream);
 }
 
 // ------------------------------------------------------------------ PPO (NEXT-2) --

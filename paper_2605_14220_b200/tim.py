@@ -87,6 +87,9 @@ _SIGS = {
     "tim_logprob_rmsnorm": (_I32, [_P, _I64, _P, _F, _P, _I32, _I32, _P, _I64, _F, _P, _P, _P, _P, _SZ, _P, _P]),
     "tim_head_backward_workspace_bytes": (_SZ, [_I64, _I32, _I32]),
     "tim_head_backward": (_I32, [_P, _I64, _P, _I32, _I32, _P, _I64, _F, _P, _P, _P, _P, _P, _P, _SZ, _P, _P]),
+    "tim_logprob_saved": (_I32, [_P, _I64, _P, _I32, _I32, _P, _I64, _F, _P, _P, _P, _P, _P, _SZ, _P, _P]),
+    "tim_head_backward_saved": (_I32, [_P, _I64, _P, _I32, _I32, _P, _I64, _F, _P, _P, _P, _P, _P, _P, _P, _P,
+                                       _SZ, _P, _P]),
     "tim_ppo_partial_bytes": (_SZ, [_I64, _I32]),
     "tim_ppo_workspace_bytes": (_SZ, [_I64, _I32, _I32]),
     "tim_ppo_loss": (_I32, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P,
@@ -360,11 +363,38 @@ def logprob_rmsnorm(hidden: torch.Tensor, gamma: torch.Tensor, weight: torch.Ten
     return lp, ent
 
 
+def logprob_saved(hidden: torch.Tensor, weight: torch.Tensor, ids: torch.Tensor, temperature: float = 1.0,
+                  temperatures: torch.Tensor | None = None, status: torch.Tensor | None = None):
+    """tim_logprob_saved: (logp, entropy, lse2) on the device; pass ``saved=(entropy, lse2)`` to
+    head_backward to skip its forward pass."""
+    dev = hidden.device
+    if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
+        raise TypeError("hidden and weight must be bfloat16")
+    if hidden.dim() != 2 or hidden.stride(1) != 1:
+        raise ValueError("hidden must be [N, d] with unit inner stride")
+    weight = weight.contiguous()
+    ids = ids.to(device=dev, dtype=torch.int64).contiguous()
+    if temperatures is not None:
+        temperatures = temperatures.to(device=dev, dtype=torch.float32).contiguous()
+    N, d = hidden.shape
+    V = weight.shape[0]
+    if weight.shape[1] != d or ids.numel() != N:
+        raise ValueError("shape mismatch")
+    lp, ent, lse2 = (torch.empty(N, dtype=torch.float32, device=dev) for _ in range(3))
+    L = lib()
+    ws = _workspace(dev, L.tim_logprob_workspace_bytes(N, d, V), "logprob")
+    _check(L.tim_logprob_saved(_ptr(hidden), hidden.stride(0), _ptr(weight), d, V, _ptr(ids), N, float(temperature),
+                               _ptr(temperatures), _ptr(lp), _ptr(ent), _ptr(lse2), _ptr(ws), ws.numel(),
+                               _ptr(status), _stream(dev)), "tim_logprob_saved")
+    return lp, ent, lse2
+
+
 def head_backward(hidden: torch.Tensor, weight: torch.Tensor, ids: torch.Tensor, grad_logp: torch.Tensor,
                   grad_entropy: torch.Tensor | None = None, temperature: float = 1.0,
                   temperatures: torch.Tensor | None = None, need_dhidden: bool = True, need_dweight: bool = True,
-                  status: torch.Tensor | None = None):
-    """Backward of the head for L = sum_t grad_logp[t] logp_t + grad_entropy[t] H_t -- tim_head_backward.
+                  status: torch.Tensor | None = None, saved: tuple | None = None):
+    """Backward of the head for L = sum_t grad_logp[t] logp_t + grad_entropy[t] H_t -- tim_head_backward,
+    or tim_head_backward_saved when ``saved`` = (entropy, lse2) from logprob_saved on the same inputs.
 
     Returns (dhidden fp32 [N, d] or None, dweight fp32 [V, d] or None)."""
     dev = hidden.device
@@ -387,9 +417,19 @@ def head_backward(hidden: torch.Tensor, weight: torch.Tensor, ids: torch.Tensor,
     dw = torch.empty(V, d, dtype=torch.float32, device=dev) if need_dweight else None
     L = lib()
     ws = _workspace(dev, L.tim_head_backward_workspace_bytes(N, d, V), "head_backward")
-    _check(L.tim_head_backward(_ptr(hidden), hidden.stride(0), _ptr(weight), d, V, _ptr(ids), N, float(temperature),
-                               _ptr(temperatures), _ptr(grad_logp), _ptr(grad_entropy), _ptr(dh), _ptr(dw), _ptr(ws),
-                               ws.numel(), _ptr(status), _stream(dev)), "tim_head_backward")
+    if saved is None:
+        _check(L.tim_head_backward(_ptr(hidden), hidden.stride(0), _ptr(weight), d, V, _ptr(ids), N,
+                                   float(temperature), _ptr(temperatures), _ptr(grad_logp), _ptr(grad_entropy),
+                                   _ptr(dh), _ptr(dw), _ptr(ws), ws.numel(), _ptr(status), _stream(dev)),
+               "tim_head_backward")
+    else:
+        ent, lse2 = (x.to(device=dev, dtype=torch.float32).contiguous() for x in saved)
+        if ent.numel() != N or lse2.numel() != N:
+            raise ValueError("saved (entropy, lse2) must have one value per token")
+        _check(L.tim_head_backward_saved(_ptr(hidden), hidden.stride(0), _ptr(weight), d, V, _ptr(ids), N,
+                                         float(temperature), _ptr(temperatures), _ptr(ent), _ptr(lse2),
+                                         _ptr(grad_logp), _ptr(grad_entropy), _ptr(dh), _ptr(dw), _ptr(ws),
+                                         ws.numel(), _ptr(status), _stream(dev)), "tim_head_backward_saved")
     return dh, dw
 
 

@@ -89,6 +89,13 @@ def test_head_backward_argument_errors_are_synchronous(L):
     assert _bw(L, dh=P(68)) == 3 and _bw(L, ws=P(4096 + 16)) == 3
     assert _bw(L, wsb=1000) == 5
     assert _bw(L, n=0, dw=None) == 0                   # empty batch, dhidden only: nothing to do
+    # saved-forward variants: the saved per-token values are required
+    assert L.tim_head_backward_saved(P(4096), 256, P(8192), 256, 1024, P(16), 10, 1.0, None, None, P(256), P(32),
+                                     None, P(64), P(128), P(1 << 20), 1 << 40, None, None) == 1
+    assert L.tim_head_backward_saved(P(4096), 256, P(8192), 256, 1024, P(16), 10, 1.0, None, P(256), None, P(32),
+                                     None, P(64), P(128), P(1 << 20), 1 << 40, None, None) == 1
+    assert L.tim_logprob_saved(P(4096), 256, P(8192), 256, 1024, P(16), 10, 1.0, None, P(32), P(64), None,
+                               P(1 << 20), 1 << 30, None, None) == 1
     # workspace: forward partials + 3 per-token vectors + one bf16 G block of <= 4 GiB
     nb = (1 << 32) // (2 * 151936) // 256 * 256
     assert nb == 14080

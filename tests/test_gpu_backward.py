@@ -103,3 +103,31 @@ def test_token_blocks_and_status(tim):
     tim.head_backward(H, W, bad, gl, ge, status=st)
     code, idx = tim.read_status(st)
     assert code == 9 and idx == 14300, (code, idx)
+
+
+def _lse2_oracle(H, W, T):
+    """log2-sum-exp of y = z / T_t (in log2 units), fp64 from oracle.logprob.logits."""
+    from oracle.logprob import logits
+    x = logits(H.cpu(), W.cpu()) / T.cpu().double().numpy()[:, None]
+    m = x.max(axis=1)
+    return (m + np.log(np.exp(x - m[:, None]).sum(axis=1))) / np.log(2.0)
+
+
+@pytest.mark.parametrize("N,d,V", [(300, 256, 5000), (14500, 128, 151936)])
+def test_saved_forward_backward(tim, N, d, V):
+    """tim_logprob_saved: logp / entropy bitwise those of tim_logprob, lse2 within the logp
+    tolerance of the fp64 definition; tim_head_backward_saved: bitwise tim_head_backward (the
+    forward is batch-invariant, so the saved per-token values are the ones it would recompute),
+    also across the 14080-row token blocks."""
+    H, W, ids, gl, ge, T = _problem(N, d, V, 5 + N)
+    lp, ent, lse2 = tim.logprob_saved(H, W, ids, 1.0, T)
+    lp0, ent0 = tim.logprob(H, W, ids, 1.0, T)
+    assert torch.equal(lp.view(torch.int32), lp0.view(torch.int32))
+    assert torch.equal(ent.view(torch.int32), ent0.view(torch.int32))
+    rows = slice(0, 300)
+    ref = _lse2_oracle(H[rows], W, T[rows])
+    assert np.abs(lse2[rows].cpu().double().numpy() - ref).max() <= 2e-3
+    a = tim.head_backward(H, W, ids, gl, ge, 1.0, T)
+    b = tim.head_backward(H, W, ids, gl, ge, 1.0, T, saved=(ent, lse2))
+    for x, y in zip(a, b):
+        assert torch.equal(x.view(torch.int32), y.view(torch.int32))
