@@ -24,6 +24,11 @@ tim_status tim_debug_logprob_logits(const void* hidden_bf16, int64_t ld_hidden, 
  * persistent grid (emulates a GPU with fewer SMs for batch-invariance tests), 0 = all SMs. */
 tim_status tim_debug_set_kernel(int32_t use_pair, int32_t max_ctas_or_clusters);
 
+/* Small-batch H staging (n_tok < 256, not a multiple of 128): 1 = copy the rows into zero-padded
+ * whole 128-row boxes in the workspace before the kernel (default), 0 = let TMA zero-fill the
+ * partial box on every load.  Never changes a result bit (rows are independent). */
+tim_status tim_debug_set_pad_small(int32_t enable);
+
 /* Performance knobs (never change results): L2 eviction policy of the hidden-state (H) and
  * weight (W) TMA tile loads, 0 = no hint, 1 = evict_normal, 2 = evict_first, 3 = evict_last;
  * sleep_waits = 1 makes the TMA-producer and epilogue mbarrier waits sleep in hardware;

@@ -33,6 +33,7 @@ std::mutex g_mu;
 
 // debug knobs (tim_debug.h): kernel variant and an SM cap to emulate smaller GPUs
 int g_use_pair = 1;
+int g_pad_small = 1;
 int g_max_clusters = 0;
 // tuning knobs (tim_debug.h): L2 policies of the H / W tile loads and sleeping mbarrier waits
 int g_h_policy = 3;  // H tiles: evict_last (re-read for every vocab tile of the sweep)
@@ -150,12 +151,30 @@ int pick_group(const DevInfo* dev, bool pair, int n_slices, int64_t groups, int3
   return g;
 }
 
+// Small batches whose last 128-row H box is mostly out of bounds (n_tok < 256, n_tok % 128 in
+// [1, 32]): the kernel would re-load that box (TMA zero-fills the missing rows) for every vocab tile
+// and K step, and such boxes are slow to fill (C1's head, interleaved in one process: N = 1
+// 0.26 ms, N = 16 0.17-0.22 ms, N = 64 0.13 ms).  Their rows are copied into a zero-padded buffer
+// of whole boxes at the end of the workspace first (one small kernel, ~4 us: N = 1 0.16 ms, N = 16
+// 0.13-0.16 ms); above 32 rows the copy costs more than it saves.  Rows are independent, so no
+// result bit changes (tested).
+static int64_t small_pad_rows(int64_t n_tok) {
+  if (n_tok <= 0 || n_tok >= 256 || n_tok % 128 == 0 || n_tok % 128 > 32) return 0;
+  return (n_tok + 127) / 128 * 128;
+}
+static size_t small_pad_bytes(int64_t n_tok, int32_t hidden) {
+  const int64_t r = small_pad_rows(n_tok);
+  if (r == 0 || hidden < 1) return 0;
+  return 256 + static_cast<size_t>(r) * static_cast<size_t>(hidden) * 2u;  // + alignment slack
+}
+
 tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weight, int32_t d, int32_t vocab,
                         const int64_t* ids, int64_t n_tok, float temperature, const float* temps, float* logp,
                         float* ent, void* ws, size_t ws_bytes, tim_device_status* dstatus, void* stream,
                         float* debug_logits, int64_t debug_ld, const uint64_t* row_keys = nullptr,
                         uint64_t seed = 0, int64_t* ids_out = nullptr, int32_t tp = 1, int32_t tp_rank = 0,
-                        void* tp_partial_out = nullptr, float* lse2_out = nullptr, int64_t index_base = 0) {
+                        void* tp_partial_out = nullptr, float* lse2_out = nullptr, int64_t index_base = 0,
+                        bool pad_small = true) {
   const bool sample = row_keys != nullptr;
   const bool tp_mode = tp_partial_out != nullptr;  // vocab-parallel rank: partials only, no merge
   if (!weight) return TIM_ERR_NULL;
@@ -170,9 +189,11 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   if (!aligned(hidden, 16)) return TIM_ERR_ALIGN;
   if (!ws) return TIM_ERR_NULL;
   if (!aligned(ws, 16)) return TIM_ERR_ALIGN;
+  const bool pad = pad_small && g_pad_small && !tp_mode && small_pad_rows(n_tok) > 0;
   const size_t ws_need = tp_mode ? kWsHeaderBytes
                                  : (sample ? tim_sample_workspace_bytes(n_tok, d, vocab)
-                                           : tim_logprob_workspace_bytes(n_tok, d, vocab));
+                                           : tim_logprob_workspace_bytes(n_tok, d, vocab)) -
+                                       (pad ? 0 : small_pad_bytes(n_tok, d));
   if (ws_bytes < ws_need) return TIM_ERR_WORKSPACE;
   // fixed split of the full vocabulary; a tensor-parallel rank owns slices [s0, s1) = W rows [row0, row1)
   const int32_t S_total = vocab_slices(vocab);
@@ -191,13 +212,26 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   // otherwise 1-pair clusters with M-tile groups (below).  Never changes a result bit.
   const bool quad = pair && g_quad != 0 && dev->max_pair_clusters >= 2 &&
                     dev->max_pair_clusters * 256.0 * d * 2.0 <= 0.75 * dev->l2_bytes;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* wsb = static_cast<uint8_t*>(ws);
+  const void* h_tma = hidden;
+  int64_t h_ld = ld_hidden, h_rows = n_tok;
+  if (pad) {
+    const size_t off = (ws_need - small_pad_bytes(n_tok, d) + 255) & ~size_t(255);
+    uint8_t* hp = wsb + off;
+    h_rows = small_pad_rows(n_tok);
+    h_ld = d;
+    const size_t row_b = static_cast<size_t>(d) * 2u;
+    if (launch_pad_rows(hidden, ld_hidden * 2, hp, static_cast<int>(row_b), static_cast<int>(n_tok),
+                        static_cast<int>(h_rows), s) != cudaSuccess)
+      return TIM_ERR_CUDA;
+    h_tma = hp;
+  }
   CUtensorMap th, tw;
-  if (!encode_bf16_2d(&th, hidden, n_tok, d, ld_hidden, 128)) return TIM_ERR_CUDA;
+  if (!encode_bf16_2d(&th, h_tma, h_rows, d, h_ld, 128)) return TIM_ERR_CUDA;
   if (!encode_bf16_2d(&tw, weight, row1 - row0, d, d, quad ? fwd_w_box_rows(pair) / 2 : fwd_w_box_rows(pair)))
     return TIM_ERR_CUDA;
 
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  uint8_t* wsb = static_cast<uint8_t*>(ws);
   WsHeader* hdr = reinterpret_cast<WsHeader*>(wsb);
   float4* partials = tp_mode ? static_cast<float4*>(tp_partial_out) : reinterpret_cast<float4*>(wsb + kWsHeaderBytes);
   if (cudaMemsetAsync(hdr, 0, kWsHeaderBytes, s) != cudaSuccess) return TIM_ERR_CUDA;
@@ -224,8 +258,8 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   p.sleep_waits = g_sleep_waits;
   p.progress = reinterpret_cast<uint32_t*>(wsb + kWsProgressOffset);
   p.sync_slack = g_sync_slack;
-  p.hidden_ptr = hidden;
-  p.ld_hidden_bytes = ld_hidden * 2;
+  p.hidden_ptr = h_tma;
+  p.ld_hidden_bytes = h_ld * 2;
   p.demote = g_demote;
   p.row_keys = row_keys;
   p.seed = seed;
@@ -416,9 +450,9 @@ int tim_abi_version(void) { return TIM_ABI_VERSION; }
 int32_t tim_logprob_vocab_slices(int32_t vocab) { return vocab < 1 ? 0 : vocab_slices(vocab); }
 
 size_t tim_logprob_workspace_bytes(int64_t n_tok, int32_t hidden, int32_t vocab) {
-  (void)hidden;
   if (n_tok < 0 || vocab < 1) return 0;
-  return kWsHeaderBytes + static_cast<size_t>(vocab_slices(vocab)) * static_cast<size_t>(n_tok) * 16u;
+  return kWsHeaderBytes + static_cast<size_t>(vocab_slices(vocab)) * static_cast<size_t>(n_tok) * 16u +
+         small_pad_bytes(n_tok, hidden);
 }
 
 tim_status tim_logprob(const void* hidden_bf16, int64_t ld_hidden, const void* weight_bf16, int32_t hidden,
@@ -431,9 +465,9 @@ tim_status tim_logprob(const void* hidden_bf16, int64_t ld_hidden, const void* w
 }
 
 size_t tim_sample_workspace_bytes(int64_t n_tok, int32_t hidden, int32_t vocab) {
-  (void)hidden;
   if (n_tok < 0 || vocab < 1) return 0;
-  return kWsHeaderBytes + 2u * static_cast<size_t>(vocab_slices(vocab)) * static_cast<size_t>(n_tok) * 16u;
+  return kWsHeaderBytes + 2u * static_cast<size_t>(vocab_slices(vocab)) * static_cast<size_t>(n_tok) * 16u +
+         small_pad_bytes(n_tok, hidden);
 }
 
 tim_status tim_sample(const void* hidden_bf16, int64_t ld_hidden, const void* weight_bf16, int32_t hidden,
@@ -855,7 +889,7 @@ static tim_status head_backward_impl(const void* hidden_bf16, int64_t ld_hidden,
     if (!saved) {
       st = logprob_impl(hb, ld_hidden, weight_bf16, d, vocab, token_ids + b0, nbc, temperature, tb, logp, ent_ws,
                         fwd_ws, fwd_bytes, dstatus, stream, nullptr, 0, nullptr, 0, nullptr, 1, 0, nullptr, lse2_ws,
-                        b0);
+                        b0, /*pad_small=*/false);
       if (st != TIM_OK) return st;
     }
     // (2) recompute the logits tile by tile; the epilogue writes G = dL/dz (bf16) instead of LSE partials
@@ -1082,6 +1116,12 @@ tim_status tim_debug_logprob_logits(const void* hidden_bf16, int64_t ld_hidden, 
   if (ld_logits < vocab) return TIM_ERR_SHAPE;
   return logprob_impl(hidden_bf16, ld_hidden, weight_bf16, hidden, vocab, token_ids, n_tok, 1.0f, nullptr, logp_out,
                       entropy_out, workspace, workspace_bytes, nullptr, stream, logits_out, ld_logits);
+}
+
+tim_status tim_debug_set_pad_small(int32_t enable) {
+  if (enable != 0 && enable != 1) return TIM_ERR_VALUE;
+  g_pad_small = enable;
+  return TIM_OK;
 }
 
 tim_status tim_debug_set_kernel(int32_t use_pair, int32_t max_ctas_or_clusters) {

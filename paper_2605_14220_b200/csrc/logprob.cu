@@ -654,6 +654,23 @@ static cudaError_t launch_fwd(const CUtensorMap& th, const CUtensorMap& tw, cons
 int fwd_unit_rows(bool pair) { return pair ? KCfg<true>::kUnitM : KCfg<false>::kUnitM; }
 int fwd_w_box_rows(bool pair) { return pair ? KCfg<true>::kBRows : KCfg<false>::kBRows; }
 
+// Small-batch H staging (api.cu small_pad_rows): rows [0, n_tok) copied, rows [n_tok, n_rows)
+// zeroed, one block per row, 16-B vectors.  Pure data movement.
+__global__ void __launch_bounds__(256) pad_rows_kernel(const uint8_t* __restrict__ src, int64_t ld_src_bytes,
+                                                       uint8_t* __restrict__ dst, int row_bytes, int n_tok) {
+  const int row = blockIdx.x;
+  uint4* d = reinterpret_cast<uint4*>(dst + static_cast<int64_t>(row) * row_bytes);
+  const uint4* sp = reinterpret_cast<const uint4*>(src + static_cast<int64_t>(row) * ld_src_bytes);
+  for (int i = threadIdx.x; i < row_bytes / 16; i += blockDim.x)
+    d[i] = row < n_tok ? __ldg(sp + i) : make_uint4(0u, 0u, 0u, 0u);
+}
+cudaError_t launch_pad_rows(const void* src, int64_t ld_src_bytes, void* dst, int row_bytes, int n_tok, int n_rows,
+                            cudaStream_t stream) {
+  pad_rows_kernel<<<n_rows, 256, 0, stream>>>(static_cast<const uint8_t*>(src), ld_src_bytes,
+                                              static_cast<uint8_t*>(dst), row_bytes, n_tok);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_head_grad(const CUtensorMap& th, const CUtensorMap& tw, const CUtensorMap& tg,
                              const LogprobParams& p, int grid, cudaStream_t stream) {
   return launch_fwd<true, false, false, 1, true>(th, tw, p, grid, stream, &tg);

@@ -110,6 +110,8 @@ int fwd_w_box_rows(bool pair);
 cudaError_t launch_logprob_fwd(bool pair, bool debug, bool sample, bool quad, const CUtensorMap& th,
                                const CUtensorMap& tw, const LogprobParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_logprob_merge(const MergeParams& p, cudaStream_t stream);
+cudaError_t launch_pad_rows(const void* src, int64_t ld_src_bytes, void* dst, int row_bytes, int n_tok, int n_rows,
+                            cudaStream_t stream);
 cudaError_t launch_head_grad(const CUtensorMap& th, const CUtensorMap& tw, const CUtensorMap& tg,
                              const LogprobParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_sample_merge(const MergeParams& p, cudaStream_t stream);

@@ -102,6 +102,7 @@ _SIGS = {
     "tim_comm_destroy": (_I32, [_P]),
     "tim_debug_logprob_logits": (_I32, [_P, _I64, _P, _I32, _I32, _P, _I64, _P, _I64, _P, _P, _P, _SZ, _P]),
     "tim_debug_set_kernel": (_I32, [_I32, _I32]),
+    "tim_debug_set_pad_small": (_I32, [_I32]),
     "tim_debug_set_tuning": (_I32, [_I32, _I32, _I32, _I32]),
     "tim_debug_set_schedule": (_I32, [_I32, _I32]),
     "tim_debug_set_cluster": (_I32, [_I32]),
@@ -462,6 +463,11 @@ def debug_set_schedule(group: int = 0, demote: bool = False):
 def debug_set_cluster(pairs_per_cluster: int = 1):
     """Cluster shape knob (results unchanged): 2 = two CTA pairs sharing W through TMA multicast."""
     _check(lib().tim_debug_set_cluster(int(pairs_per_cluster)), "tim_debug_set_cluster")
+
+
+def debug_set_pad_small(enable: bool = True):
+    """Small-batch H staging knob (tim_debug_set_pad_small); never changes a result bit."""
+    _check(lib().tim_debug_set_pad_small(1 if enable else 0), "tim_debug_set_pad_small")
 
 
 def debug_set_kernel(use_pair: bool = True, max_ctas: int = 0):

@@ -49,6 +49,13 @@ def test_workspace_sizes(L):
     assert L.tim_logprob_vocab_slices(1024) == 4      # 4 tiles of 256 -> 4 slices
     assert L.tim_logprob_vocab_slices(1) == 1
     assert L.tim_logprob_workspace_bytes(1000, 2048, 151936) == 1024 + 64 * 1000 * 16
+    # n_tok < 256 with n_tok % 128 in [1, 32]: + a zero-padded copy of H in whole 128-row boxes
+    assert L.tim_logprob_workspace_bytes(20, 2048, 151936) == 1024 + 64 * 20 * 16 + 256 + 128 * 2048 * 2
+    assert L.tim_logprob_workspace_bytes(130, 256, 1024) == 1024 + 4 * 130 * 16 + 256 + 256 * 256 * 2
+    assert L.tim_logprob_workspace_bytes(100, 2048, 151936) == 1024 + 64 * 100 * 16
+    assert L.tim_logprob_workspace_bytes(128, 2048, 151936) == 1024 + 64 * 128 * 16
+    assert L.tim_logprob_workspace_bytes(300, 2048, 151936) == 1024 + 64 * 300 * 16
+    assert L.tim_sample_workspace_bytes(1, 64, 1024) == 1024 + 2 * 4 * 16 + 256 + 128 * 64 * 2
     assert L.tim_correct_partial_bytes(5) == 128 + 5 * 32
     assert L.tim_correct_workspace_bytes(100, 5, 1) == 512 * 2
     assert L.tim_correct_workspace_bytes(100, 5, 4) == 512 * 5
