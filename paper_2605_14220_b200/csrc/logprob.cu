@@ -244,10 +244,11 @@ __device__ __noinline__ uint32_t wait_progress(const uint32_t* prog, uint32_t nc
 // (row-major, ld = p.g_ld) for the two library GEMMs dH = G W and dW = G^T H: each warp stages
 // its 32 rows x 32 columns in shared memory and one lane writes the tile with a TMA store
 // (tmap_g), instead of 32 scattered 64-B row segments per chunk.
-__device__ __forceinline__ void grad_chunk(const uint32_t (&r)[32], float c, int col0, int vocab, int64_t a,
-                                           float gl, float ge, float gH, float lse2, float invT, uint32_t stage,
-                                           int lane) {
-  constexpr float kLn2 = 0.69314718055994530942f;
+// G[t, v] = (g (1[v = a] - p) - e p (ln p + H)) / T per logit, with the row constants folded
+// (gA = -e ln2 / T, gB = (-g - e H) / T, gS = g / T):  G = p (gA log2 p + gB) + 1[v = a] gS --
+// two FFMAs, an EX2 and a select per logit; `rel` = a - col0 when a falls in this chunk, else -1.
+__device__ __forceinline__ void grad_chunk(const uint32_t (&r)[32], float c, int rel, float gA, float gB, float gS,
+                                           float lse2, uint32_t stage, int lane) {
   uint32_t packed[16];
 #pragma unroll
   for (int i = 0; i < 32; i += 2) {
@@ -256,14 +257,11 @@ __device__ __forceinline__ void grad_chunk(const uint32_t (&r)[32], float c, int
     for (int q = 0; q < 2; ++q) {
       const float t = fmaf(__uint_as_float(r[i + q]), c, -lse2);  // log2 p
       const float pr = ex2_approx(t);
-      float g = pr * (-gl - ge * fmaf(t, kLn2, gH));
-      if (a == col0 + i + q) g += gl;
-      gv[q] = g * invT;
+      gv[q] = fmaf(pr, fmaf(t, gA, gB), rel == i + q ? gS : 0.f);
     }
     const __nv_bfloat162 b = __floats2bfloat162_rn(gv[0], gv[1]);
     packed[i / 2] = *reinterpret_cast<const uint32_t*>(&b);
   }
-  (void)vocab;
   // this row's 64 B into the warp's 32 x 32 bf16 staging tile, 16-B chunks swizzled as the
   // tensor map's SWIZZLE_64B expects (chunk ^ ((row >> 1) & 3)): conflict-free shared stores
 #pragma unroll
@@ -465,13 +463,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float T = (valid && p.temps) ? __ldg(p.temps + row) : p.temperature;
       const float c = __fdiv_rn(kLog2eF, T);
       float m = -CUDART_INF_F, s = 0.f, uu = 0.f, ya = -CUDART_INF_F;
-      float gl = 0.f, ge = 0.f, gH = 0.f, lse2 = 0.f, invT = 0.f;  // gradient mode (NEXT-3)
+      float gA = 0.f, gB = 0.f, gS = 0.f, lse2 = 0.f;  // gradient mode (NEXT-3): grad_chunk's row constants
       if (kGrad && valid) {
-        gl = __ldg(p.grad_logp + row);
-        ge = p.grad_ent ? __ldg(p.grad_ent + row) : 0.f;
-        gH = __ldg(p.ent_in + row);
+        const float gl = __ldg(p.grad_logp + row);
+        const float ge = p.grad_ent ? __ldg(p.grad_ent + row) : 0.f;
+        const float gH = __ldg(p.ent_in + row);
+        const float invT = __fdiv_rn(1.0f, T);
+        constexpr float kLn2 = 0.69314718055994530942f;
         lse2 = __ldg(p.lse2_in + row);
-        invT = __fdiv_rn(1.0f, T);
+        gA = -ge * kLn2 * invT;
+        gB = (-gl - ge * gH) * invT;
+        gS = gl * invT;
       }
       float best_s = -CUDART_INF_F, best_y = -CUDART_INF_F;
       int best_col = -1;
@@ -509,11 +511,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t stage = gstage0 + gbuf * 2048u;
             if (lane == 0) bulk_wait_group_read<1>();  // this buffer's previous store has read it
             __syncwarp();
-            grad_chunk(r, c, col0, p.vocab, a, gl, ge, gH, lse2, invT, stage, lane);
+            const int64_t rel64 = a - col0;
+            grad_chunk(r, c, static_cast<uint64_t>(rel64) < 32u ? static_cast<int>(rel64) : -1, gA, gB, gS, lse2,
+                       stage, lane);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(&tmap_g, stage, col0 - p.g_col0, row - lane);
+              // G streams out (4 GiB per block): evict_first keeps the W slice resident in L2
+              tma_store_2d_hint(&tmap_g, stage, col0 - p.g_col0, row - lane, policy_evict_first());
               bulk_commit_group();
             }
             gbuf ^= 1;
