@@ -279,6 +279,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                        const __grid_constant__ CUtensorMap tmap_g, LogprobParams p) {
   using C = KCfg<kPair>;
   static_assert(kNP == 1 || (kPair && kNP == 2), "multicast clusters are built from CTA pairs");
+#ifndef TIM_EPI_PREFETCH
+#define TIM_EPI_PREFETCH 0
+#endif
+  // software-pipelined TMEM loads in the epilogue (0 = off, the default: measured slower for the
+  // sampling twin and neutral for the forward); 1 = sampling twin, 2 = also the forward
+  constexpr bool kPrefetch = !kGrad && !kDebug && (kSample ? TIM_EPI_PREFETCH >= 1 : TIM_EPI_PREFETCH >= 2);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
@@ -490,16 +496,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kTileN;
         const bool tail_tile = (vt + 1) * kTileN > p.vocab;
-#pragma unroll 1
-        for (int ch = 0; ch < kTileN / 32; ++ch) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(taddr + ch * 32, r);
-          tmem_ld_wait();
-          if (ch == kTileN / 32 - 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
-          }
+        auto chunk = [&](const uint32_t (&r)[32], int ch) {
           const int col0 = vt * kTileN + ch * 32;
           if (kDebug && valid) {
             float* dst = p.debug_logits + static_cast<int64_t>(row) * p.debug_ld + col0;
@@ -532,6 +529,35 @@ __global__ void __launch_bounds__(kThreads, 1)
               gumbel_chunk<true>(r, c, col0, p.vocab, keys, rk_lo, rk_hi, best_s, best_y, best_col);
             else
               gumbel_chunk<false>(r, c, col0, p.vocab, keys, rk_lo, rk_hi, best_s, best_y, best_col);
+          }
+        };
+        auto release = [&]() {  // every TMEM load of this tile has landed: the MMA may overwrite it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+        };
+        if constexpr (kPrefetch) {
+          // the next chunk's TMEM load is in flight while this chunk computes
+          uint32_t ra[32], rb[32];
+          tmem_ld_32x32b_x32(taddr, ra);
+#pragma unroll 1
+          for (int ch = 0; ch < kTileN / 32; ch += 2) {
+            tmem_ld_wait_regs(ra);
+            tmem_ld_32x32b_x32(taddr + (ch + 1) * 32, rb);
+            chunk(ra, ch);
+            tmem_ld_wait_regs(rb);
+            if (ch + 2 < kTileN / 32) tmem_ld_32x32b_x32(taddr + (ch + 2) * 32, ra);
+            else release();
+            chunk(rb, ch + 1);
+          }
+        } else {
+#pragma unroll 1
+          for (int ch = 0; ch < kTileN / 32; ++ch) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(taddr + ch * 32, r);
+            tmem_ld_wait();
+            if (ch == kTileN / 32 - 1) release();
+            chunk(r, ch);
           }
         }
         acc ^= 1;
