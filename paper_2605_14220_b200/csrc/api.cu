@@ -38,7 +38,7 @@ int g_max_clusters = 0;
 // tuning knobs (tim_debug.h): L2 policies of the H / W tile loads and sleeping mbarrier waits
 int g_h_policy = 3;  // H tiles: evict_last (re-read for every vocab tile of the sweep)
 int g_w_policy = 2;  // W tiles: evict_first (shared by all pairs within a few tiles, then dead)
-int g_sleep_waits = 1;
+int g_sleep_waits = 0;  // spinning mbarrier waits: +0.7-1% on C1 / C2 / sampling vs nanosleep (profiles/r01_sleep_waits_ab.txt)
 int g_sync_slack = 4;  // pairs stay within 4 vocab tiles of each other: W window ~4 MB in L2
 int g_group = 0;       // pairs per M-tile group (0 = automatic from the L2 size)
 int g_demote = 0;      // demote finished H tiles to evict_normal (applypriority)
