@@ -31,7 +31,10 @@ constexpr int kTpl = 4;                 // tokens per lane (one float4 of num / 
 constexpr int kWarpTok = 32 * kTpl;     // tokens per warp chunk
 constexpr int kLocalThreads = 128;
 constexpr int kLocalWarps = kLocalThreads / 32;
-constexpr int kStages = 4;              // per-warp TMA ring: chunks of num / den in flight
+#ifndef TIM_CORR_STAGES
+#define TIM_CORR_STAGES 4
+#endif
+constexpr int kStages = TIM_CORR_STAGES;  // per-warp TMA ring: chunks of num / den in flight
 constexpr int kFoldChunks = 16;        // the exact fp64 chunk sums are folded into int128 this often
 
 // Per-thread state that the fast path does not touch every chunk, in shared memory so the hot

@@ -28,7 +28,7 @@ def timed(fn, reps=4):
     return a.elapsed_time(b) / reps, out
 
 
-knobs = [(3, 2, 1, 4), (3, 2, 1, 0), (3, 2, 1, 16), (3, 2, 0, 4), (3, 2, 1, 2)]
+knobs = [tuple(int(x) for x in k.split(",")) for k in os.environ.get("KNOBS", "3,2,0,4 3,2,1,4 3,2,0,0 3,2,0,16 3,2,0,2").split()]
 for rep in range(2):
     for k in knobs:
         tim.debug_set_tuning(*k)
