@@ -100,7 +100,7 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 3])
 def test_two_rank_exchange_reproduces_single_process(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -114,5 +114,8 @@ def test_two_rank_exchange_reproduces_single_process(world):
         assert p.exitcode == 0
     res.sort()
     assert all(ok for _, ok, _, _ in res), res
-    assert res[0][3][1] == res[1][3][0] and res[0][3][1] not in (0, 900, 1500, 1501, 3900, 5000)  # cut mid-sequence
-    assert res[0][2] == res[1][2]
+    bounds = (0, 900, 1500, 1501, 3900, 5000, 7001)
+    for r in range(world - 1):
+        assert res[r][3][1] == res[r + 1][3][0]
+    assert any(res[r][3][1] not in bounds for r in range(world - 1))   # a cut falls mid-sequence
+    assert len({k for _, _, k, _ in res}) == 1
