@@ -20,6 +20,9 @@ roll = synth.perturb_laplace_mix(lp, 3)
 res = tim.correct(lp, roll, cu, tim.PRESETS["tis-srs-k3-corr-ratio"], mask)
 pp = tim.ppo_loss(lp, roll, torch.randn(300, device=dev), cu, tim.PPOConfig(), coeff=res["coeff"])
 dh, dw = tim.head_backward(H, W, ids, torch.ones(300, device=dev), torch.full((300,), 0.01, device=dev))
+lps, ents, lse2 = tim.logprob_saved(H, W, ids)
+dh2, dw2 = tim.head_backward(H, W, ids, torch.ones(300, device=dev), saved=(ents, lse2))
+lp5, _ = tim.logprob(H[:5], W, ids[:5])                       # small-batch H staging (pad_rows_kernel)
 torch.cuda.synchronize()
 print("sanitize run ok", float(lp.sum()), res["stats"]["n_seq_rejected"], pp["stats"]["n_clipped"], float(dh.abs().sum()))
 # a larger correction / PPO call: several chunks per warp, so the per-warp TMA ring of the
