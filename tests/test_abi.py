@@ -185,3 +185,13 @@ def test_missing_library_fails_loudly():
     env = dict(os.environ, TIM_LIBRARY=os.path.join(ROOT, "no_such_libtim.so"))
     r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
     assert "raised True" in r.stdout, r.stdout + r.stderr
+
+
+def test_debug_knobs_validate_arguments(L):
+    """Performance knobs reject out-of-range values synchronously and accept their defaults."""
+    assert L.tim_debug_set_pad_small(2) == 4 and L.tim_debug_set_pad_small(-1) == 4
+    assert L.tim_debug_set_pad_small(1) == 0
+    assert L.tim_debug_set_tuning(4, 2, 0, 4) == 4 and L.tim_debug_set_tuning(3, 2, 0, -1) == 4
+    assert L.tim_debug_set_tuning(3, 2, 0, 4) == 0          # the defaults
+    assert L.tim_debug_set_kernel(2, 0) == 4 and L.tim_debug_set_kernel(1, -1) == 4
+    assert L.tim_debug_set_kernel(1, 0) == 0
