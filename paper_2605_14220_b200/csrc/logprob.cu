@@ -84,17 +84,28 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float c, int 
     m = cmax;
   }
   const float nm = -m;
-  float s4[4] = {0.f, 0.f, 0.f, 0.f}, u4[4] = {0.f, 0.f, 0.f, 0.f};
+  // four partial sums per quantity (column i goes to i mod 4, ascending i), two at a time in
+  // packed fp32 pairs: the same per-lane operations as four scalar chains
+  float2 s01 = make_float2(0.f, 0.f), s23 = s01, u01 = s01, u23 = s01;
+  const float2 c2 = make_float2(c, c), nm2 = make_float2(nm, nm);
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    float t = fmaf(z[i], c, nm);
-    if (kTail) t = fmaxf(t, -256.f);  // masked column: e = 0, e * t = 0 (no -inf * 0)
-    const float e = ex2_approx(t);
-    s4[i & 3] += e;
-    u4[i & 3] = fmaf(e, t, u4[i & 3]);
+  for (int i = 0; i < 32; i += 2) {
+    float2 t = ffma2(make_float2(z[i], z[i + 1]), c2, nm2);
+    if (kTail) {  // masked column: e = 0, e * t = 0 (no -inf * 0)
+      t.x = fmaxf(t.x, -256.f);
+      t.y = fmaxf(t.y, -256.f);
+    }
+    const float2 e = make_float2(ex2_approx(t.x), ex2_approx(t.y));
+    if ((i & 3) == 0) {
+      s01 = fadd2(s01, e);
+      u01 = ffma2(e, t, u01);
+    } else {
+      s23 = fadd2(s23, e);
+      u23 = ffma2(e, t, u23);
+    }
   }
-  s += (s4[0] + s4[1]) + (s4[2] + s4[3]);
-  u += (u4[0] + u4[1]) + (u4[2] + u4[3]);
+  s += (s01.x + s01.y) + (s23.x + s23.y);
+  u += (u01.x + u01.y) + (u23.x + u23.y);
 }
 
 // First vocab tile of local slice j: global slice slice0 + j of the fixed split of n_vt tiles into
@@ -154,18 +165,25 @@ __device__ __forceinline__ void gumbel_chunk(const uint32_t (&r)[32], float c, i
     const uint4 x = philox4x32_10(make_uint4(static_cast<uint32_t>(col0 >> 2) + g, 0u, rk_lo, rk_hi), keys);
     const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < 4; q += 2) {
       const int i = 4 * g + q;
       // u = ((x >> 9) + 1/2) 2^-23 exactly: 1.f with the 23 mantissa bits (x >> 9), minus
-      // (1 - 2^-24) (Sterbenz: exact) -- no int->float conversion on the XU pipe
-      const float u = __uint_as_float(0x3f800000u | (xs[q] >> 9)) - 0x1.fffffep-1f;
-      const float y = __uint_as_float(r[i]) * c;
-      float sc = y - lg2_approx(-lg2_approx(u));
-      if (kTail && col0 + i >= vocab) sc = -CUDART_INF_F;
-      if (sc > best_s) {
-        best_s = sc;
-        best_y = y;
-        best_col = col0 + i;
+      // (1 - 2^-24) (Sterbenz: exact) -- no int->float conversion on the XU pipe.  Two columns
+      // per packed fp32 op (each lane the scalar IEEE op).
+      const float2 u = fsub2(make_float2(__uint_as_float(0x3f800000u | (xs[q] >> 9)),
+                                         __uint_as_float(0x3f800000u | (xs[q + 1] >> 9))),
+                             make_float2(0x1.fffffep-1f, 0x1.fffffep-1f));
+      const float2 y = fmul2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), make_float2(c, c));
+      const float2 sc = fsub2(y, make_float2(lg2_approx(-lg2_approx(u.x)), lg2_approx(-lg2_approx(u.y))));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float sch = h ? sc.y : sc.x;
+        if (kTail && col0 + i + h >= vocab) sch = -CUDART_INF_F;
+        if (sch > best_s) {
+          best_s = sch;
+          best_y = h ? y.y : y.x;
+          best_col = col0 + i + h;
+        }
       }
     }
   }
@@ -253,12 +271,13 @@ __device__ __forceinline__ void grad_chunk(const uint32_t (&r)[32], float c, int
 #pragma unroll
   for (int i = 0; i < 32; i += 2) {
     float gv[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const float t = fmaf(__uint_as_float(r[i + q]), c, -lse2);  // log2 p
-      const float pr = ex2_approx(t);
-      gv[q] = fmaf(pr, fmaf(t, gA, gB), rel == i + q ? gS : 0.f);
-    }
+    const float2 t = ffma2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), make_float2(c, c),
+                           make_float2(-lse2, -lse2));  // log2 p
+    const float2 pr = make_float2(ex2_approx(t.x), ex2_approx(t.y));
+    const float2 g2 = ffma2(pr, ffma2(t, make_float2(gA, gA), make_float2(gB, gB)),
+                            make_float2(rel == i ? gS : 0.f, rel == i + 1 ? gS : 0.f));
+    gv[0] = g2.x;
+    gv[1] = g2.y;
     const __nv_bfloat162 b = __floats2bfloat162_rn(gv[0], gv[1]);
     packed[i / 2] = *reinterpret_cast<const uint32_t*>(&b);
   }
