@@ -91,21 +91,6 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_bar) {
 }
 
 // ---------------------------------------------------------------------- TMA --
-// 1-D bulk copy global -> shared (own CTA), completion as tx-bytes on `bar`; 16-B aligned
-// addresses, size a multiple of 16.
-__device__ __forceinline__ void bulk_g2s(uint32_t smem_dst, const void* src, uint32_t bytes, uint32_t bar,
-                                         uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-      ::"r"(smem_dst), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar), "l"(policy)
-      : "memory");
-}
-// 16-B global store with an L2 cache-policy hint
-__device__ __forceinline__ void st_global_v4_hint(void* ptr, float4 v, uint64_t policy) {
-  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "f"(v.x), "f"(v.y),
-               "f"(v.z), "f"(v.w), "l"(policy)
-               : "memory");
-}
 // Warp-wide forms (converged warp, identical operands in every lane): one elected lane issues.
 __device__ __forceinline__ void mbar_arrive_expect_tx_elect(uint32_t bar, uint32_t bytes) {
   asm volatile(
@@ -114,6 +99,8 @@ __device__ __forceinline__ void mbar_arrive_expect_tx_elect(uint32_t bar, uint32
       "r"(bytes)
       : "memory");
 }
+// 1-D bulk copy global -> shared (own CTA), completion as tx-bytes on `bar`; 16-B aligned
+// addresses, size a multiple of 16
 __device__ __forceinline__ void bulk_g2s_elect(uint32_t smem_dst, const void* src, uint32_t bytes, uint32_t bar,
                                                uint64_t policy) {
   asm volatile(
@@ -180,14 +167,8 @@ __device__ __forceinline__ void tma_load_2d(uint32_t smem_dst, const void* tmap,
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1)
       : "memory");
 }
-// 2-D TMA store shared -> global (bulk-group completion), and the bulk-group waits
-__device__ __forceinline__ void tma_store_2d(const void* tmap, uint32_t smem_src, int32_t c0, int32_t c1) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                   reinterpret_cast<uint64_t>(tmap)),
-               "r"(smem_src), "r"(c0), "r"(c1)
-               : "memory");
-}
-// the same with an L2 cache-policy hint (e.g. evict_first for a streamed-out result)
+// 2-D TMA store shared -> global (bulk-group completion) with an L2 cache-policy hint (e.g.
+// evict_first for a streamed-out result), and the bulk-group waits
 __device__ __forceinline__ void tma_store_2d_hint(const void* tmap, uint32_t smem_src, int32_t c0, int32_t c1,
                                                   uint64_t policy) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
