@@ -36,7 +36,9 @@ def _ints(a) -> np.ndarray:
 
 
 def grad_logits(H, W, ids, grad_logp, grad_ent=None, temperature: float = 1.0, temperatures=None):
-    """G = dL/dz [N, V] (float64), steps 1-4."""
+    """G = dL/dz [N, V] (float64), steps 1-4.
+
+    Pinned by: test_oracle_backward.py::test_finite_differences, ::test_torch_fp64_autograd, ::test_invariants (sum_v G = 0, G = onehot - softmax at g = 1)."""
     H64, W64 = _as_f64(H), _as_f64(W)
     ids = _ints(ids)
     N = H64.shape[0]
@@ -58,7 +60,9 @@ def grad_logits(H, W, ids, grad_logp, grad_ent=None, temperature: float = 1.0, t
 
 def head_backward(H, W, ids, grad_logp, grad_ent=None, temperature: float = 1.0, temperatures=None,
                   row_chunk: int = 64):
-    """(dhidden [N, d], dweight [V, d]) in float64, step 5 over row chunks."""
+    """(dhidden [N, d], dweight [V, d]) in float64, step 5 over row chunks.
+
+    Pinned by: test_oracle_backward.py::test_finite_differences (central differences of oracle.logprob), ::test_torch_fp64_autograd."""
     H64, W64 = _as_f64(H), _as_f64(W)
     ids = _ints(ids)
     N = H64.shape[0]

@@ -83,7 +83,10 @@ class Cfg:
 
 
 def delta(lp_num, lp_den) -> np.ndarray:
-    """C.3.1: one rounded subtraction of the widened fp32 inputs."""
+    """C.3.1: one rounded subtraction of the widened fp32 inputs.
+
+    Pinned by: test_oracle_correct.py::test_table1_delta_matches_printed (PAPER.md Table 1 P:129-138), ::test_zero_mismatch_collapses_everything.
+    """
     return np.asarray(lp_num, dtype=np.float32).astype(np.float64) - \
         np.asarray(lp_den, dtype=np.float32).astype(np.float64)
 
@@ -103,7 +106,10 @@ def _k3_series(d, top: int) -> np.ndarray:
 def exp_contract(d) -> np.ndarray:
     """C.3.6 exp_c.  |d| <= 2^-2: (1 + d) + K3_series(d) with the K3 branch's own series (n = 2..9
     for |d| <= 2^-6, n = 2..15 above), i.e. e^d = 1 + d + (e^d - 1 - d).  Otherwise Cody-Waite
-    reduction + degree-13 Taylor Horner + ldexp; +inf above 709, 0 below -700."""
+    reduction + degree-13 Taylor Horner + ldexp; +inf above 709, 0 below -700.
+
+    Pinned by: test_oracle_correct.py::test_exp_contract_within_2_ulp (60-digit mpmath).
+    """
     d = np.asarray(d, dtype=np.float64)
     dd = np.where(np.isfinite(d), np.clip(d, -700.0, 709.0), 0.0)
     k = np.rint(dd * LOG2E)
@@ -126,7 +132,10 @@ def exp_contract(d) -> np.ndarray:
 def k3_contract(d) -> np.ndarray:
     """C.3.6 K3 = e^d - 1 - d = d^2 P(d): P = Horner series of RN(1/n!) with n = 2..9 for
     |d| <= 2^-6, n = 2..15 for |d| <= 2^-2 and n = 2..23 for |d| <= 1; (exp_c(d) - 1) - d
-    otherwise."""
+    otherwise.
+
+    Pinned by: test_oracle_correct.py::test_k3_contract_within_4_ulp_of_60_digit_reference, ::test_k_closed_forms.
+    """
     d = np.asarray(d, dtype=np.float64)
     ad = np.abs(d)
     tiny = ad <= SMALL
@@ -140,7 +149,10 @@ def k3_contract(d) -> np.ndarray:
 
 
 def fixed_point(K) -> tuple[np.ndarray, np.ndarray]:
-    """C.3.8: X = rint(K * 2^52) as int64; |K| > 2^10 or non-finite -> +-2^62, saturated."""
+    """C.3.8: X = rint(K * 2^52) as int64; |K| > 2^10 or non-finite -> +-2^62, saturated.
+
+    Pinned by: test_oracle_correct.py::test_fixed_point_is_round_half_even_of_exact_product (exact rationals), ::test_saturated_sequence_rejected_and_counted.
+    """
     K = np.asarray(K, dtype=np.float64)
     sat = ~(np.abs(K) <= SAT_K)
     Ks = np.where(sat, 0.0, K)
@@ -156,19 +168,35 @@ def _isum(x: np.ndarray) -> int:
 
 
 def seq_threshold(tau: float, T: int, agg: int) -> int:
-    """C.3.9 exact floor(tau * 2^52 * (T if MEAN else 1))."""
+    """C.3.9 exact floor(tau * 2^52 * (T if MEAN else 1)).
+
+    Pinned by: test_oracle_correct.py::test_mean_threshold_is_exact_rational_floor (fractions.Fraction), ::test_less_equal_edge_sum_and_mean.
+    """
     f = Fraction(tau) * (2 ** 52) * (T if agg == AGG_MEAN else 1)
     return math.floor(f)
 
 
+def outside_sequences(cu, tok_begin: int, n: int) -> np.ndarray:
+    """Reading U13b: a local token whose global index lies outside [cu[0], cu[S]) belongs to no
+    sequence -- a data error, like a non-finite log-prob.
+
+    Pinned by: test_oracle_correct.py::test_tokens_outside_the_sequences_are_a_data_error.
+    """
+    g = np.arange(tok_begin, tok_begin + n, dtype=np.int64)
+    return (g < int(cu[0])) | (g >= int(cu[-1]))
+
+
 def local_partials(lp_num, lp_den, cu_seqlens, cfg: Cfg, resp_mask=None, tok_begin: int = 0):
     """Pass 1 on one shard [tok_begin, tok_begin + n): per-token outputs and the exact
-    per-sequence / global integer partials that one rank contributes."""
+    per-sequence / global integer partials that one rank contributes.
+
+    Pinned by: test_oracle_correct.py::test_sharding_is_exact_and_order_free, ::test_table1_tis_and_k_values, ::test_token_rs_bounds_inclusive, ::test_non_finite_is_a_data_error_with_first_index, ::test_prompt_only_sequence_is_kept_and_excluded.
+    """
     cu = np.asarray(cu_seqlens, dtype=np.int64)
     S = cu.size - 1
     d = delta(lp_num, lp_den)
     n = d.size
-    bad = ~np.isfinite(d)
+    bad = ~np.isfinite(d) | outside_sequences(cu, tok_begin, n)
     if bad.any():
         raise DataError(tok_begin + int(np.argmax(bad)))
     resp = np.ones(n, bool) if resp_mask is None else (np.asarray(resp_mask) != 0)
@@ -218,7 +246,10 @@ def local_partials(lp_num, lp_den, cu_seqlens, cfg: Cfg, resp_mask=None, tok_beg
 
 
 def combine(parts):
-    """Exact combination of the (glob, seq) partials of all ranks (order-free: integers / max)."""
+    """Exact combination of the (glob, seq) partials of all ranks (order-free: integers / max).
+
+    Pinned by: test_oracle_correct.py::test_sharding_is_exact_and_order_free.
+    """
     globs = [g for g, _ in parts]
     out = {k: sum(g[k] for g in globs) for k in globs[0] if k != "max_abs_delta"}
     out["max_abs_delta"] = max(g["max_abs_delta"] for g in globs)
@@ -229,7 +260,10 @@ def combine(parts):
 
 
 def decide(seq, cfg: Cfg):
-    """C.3.9: per-sequence keep flags and scores from the combined exact partials."""
+    """C.3.9: per-sequence keep flags and scores from the combined exact partials.
+
+    Pinned by: test_oracle_correct.py::test_table1_sentence_rejected, ::test_table1_without_flip_token_kept, ::test_less_equal_edge_sum_and_mean, ::test_contract_decisions_match_exact_real_decisions (mpmath), ::test_huge_thresholds_never_reject_or_truncate.
+    """
     S = seq.shape[0]
     keep = np.ones(S, np.uint8)
     score = np.zeros(S, np.float64)
@@ -251,7 +285,10 @@ def decide(seq, cfg: Cfg):
 
 
 def finalize_stats(glob, seq_keep, n_seq: int):
-    """C.3.10: host-side statistics from exact totals."""
+    """C.3.10: host-side statistics from exact totals.
+
+    Pinned by: test_oracle_correct.py::test_zero_mismatch_collapses_everything, ::test_k1_cancels_exactly_k3_does_not.
+    """
     st = dict(glob)
     st["n_seq"] = n_seq
     st["n_seq_rejected"] = int((np.asarray(seq_keep) == 0).sum())
@@ -262,14 +299,20 @@ def finalize_stats(glob, seq_keep, n_seq: int):
 
 
 def seq_index(cu_seqlens, tok_begin: int, n: int) -> np.ndarray:
-    """Sequence id of every local token (searchsorted on the global offsets)."""
+    """Sequence id of every local token (searchsorted on the global offsets).
+
+    Pinned by: test_oracle_correct.py::test_sharding_is_exact_and_order_free (cuts inside sequences).
+    """
     cu = np.asarray(cu_seqlens, dtype=np.int64)
     g = np.arange(tok_begin, tok_begin + n, dtype=np.int64)
     return np.searchsorted(cu, g, side="right") - 1
 
 
 def correct(lp_num, lp_den, cu_seqlens, cfg: Cfg, resp_mask=None):
-    """Single-shard (P = 1) end-to-end oracle: returns a dict with every output."""
+    """Single-shard (P = 1) end-to-end oracle: returns a dict with every output.
+
+    Pinned by: every test in test_oracle_correct.py (Table 1 values, closed forms, zero mismatch, K1 cancellation, thresholds).
+    """
     tokens, glob, seq = local_partials(lp_num, lp_den, cu_seqlens, cfg, resp_mask, 0)
     glob, seq = combine([(glob, seq)])
     seq_keep, score = decide(seq, cfg)

@@ -30,6 +30,8 @@ def _as_f64(a) -> np.ndarray:
 def logprob_entropy(H, W, ids, temperature: float = 1.0, temperatures=None, row_chunk: int = 64):
     """Return (logp[N], entropy[N]) in float64.
 
+    Pinned by: test_oracle_logprob.py (V = 1 exact zero, W = 0 closed form -ln V, V = 2 -softplus, sum exp(logp) = 1, 50-digit mpmath brute force, T = 2 == H / 2 bitwise, per-token T, shift / permutation invariance, entropy bounds).
+
     H: [N, d], W: [V, d] (bf16 values; torch or numpy), ids: [N] ints in [0, V).
     temperatures: optional per-token T [N] (overrides the scalar).
     """
@@ -58,5 +60,7 @@ def logprob_entropy(H, W, ids, temperature: float = 1.0, temperatures=None, row_
 
 
 def logits(H, W, temperature: float = 1.0):
-    """fp64 scaled logits x = H W^T / T (used by GEMM bring-up tests)."""
+    """fp64 scaled logits x = H W^T / T (used by GEMM bring-up tests).
+
+    Pinned by: test_oracle_logprob.py::test_logits_equal_mpmath_dot_products_at_temperature (40-digit dot products at T = 0.7 / 1 / 2.5)."""
     return (_as_f64(H) @ _as_f64(W).T) / float(temperature)

@@ -21,6 +21,7 @@ oracle/correct.py (one RN binary64 op per step, exact integer sums):
   X = rint(loss 2^52) (saturated at |loss| > 2^10), per-sequence and batch sums exact;
   batch_loss = (sum over sequences of their loss sums) / (number of sequences with a contributing token)
 Contributing tokens: coeff != 0 when coeff is given, else resp_mask (all tokens when absent).
+Data errors (U13, U13b): a non-finite lp / advantage / coeff, or a token outside [cu[0], cu[S]).
 """
 from __future__ import annotations
 
@@ -28,7 +29,7 @@ import dataclasses
 
 import numpy as np
 
-from .correct import DataError, _isum, delta, exp_contract, fixed_point, k3_contract
+from .correct import DataError, _isum, delta, exp_contract, fixed_point, k3_contract, outside_sequences
 
 
 @dataclasses.dataclass
@@ -41,15 +42,25 @@ class PPOCfg:
 
 
 def local(lp_cur, lp_old, adv, cu_seqlens, cfg: PPOCfg, coeff=None, resp_mask=None, tok_begin: int = 0):
+    """Pass 1 on one shard: per-token loss / grad / clip flag, C(r) histogram, exact partials.
+
+    Pinned by: test_oracle_ppo.py::test_on_policy_closed_form, ::test_clip_branches_closed_form,
+    ::test_loss_is_minus_min_of_unclipped_and_clipped (mpmath), ::test_gradient_is_score_function_derivative
+    (finite differences), ::test_histogram_edges_are_exact, ::test_non_finite_advantage_is_a_data_error.
+    """
     cu = np.asarray(cu_seqlens, dtype=np.int64)
     S = cu.size - 1
     d = delta(lp_cur, lp_old)
     n = d.size
-    bad = ~np.isfinite(d)
+    A = np.asarray(adv, dtype=np.float32).astype(np.float64)
+    # data errors (reading U13): non-finite log-prob, advantage or weight; a token outside the
+    # global sequences (U13b).  The first bad global index is reported.
+    bad = ~np.isfinite(d) | ~np.isfinite(A) | outside_sequences(cu, tok_begin, n)
+    if coeff is not None:
+        bad |= ~np.isfinite(np.asarray(coeff, dtype=np.float32))
     if bad.any():
         raise DataError(tok_begin + int(np.argmax(bad)))
     r = exp_contract(d)
-    A = np.asarray(adv, dtype=np.float32).astype(np.float64)
     if coeff is not None:
         c32 = np.asarray(coeff, dtype=np.float32)
         contrib = c32 != 0
@@ -95,6 +106,10 @@ def local(lp_cur, lp_old, adv, cu_seqlens, cfg: PPOCfg, coeff=None, resp_mask=No
 
 
 def combine(parts):
+    """Exact combination of the ranks' partials (integer sums).
+
+    Pinned by: test_oracle_ppo.py::test_sharding_is_exact.
+    """
     globs = [g for g, _ in parts]
     out = {k: sum(g[k] for g in globs) for k in globs[0] if k != "hist"}
     out["hist"] = sum(g["hist"] for g in globs)
@@ -105,6 +120,10 @@ def combine(parts):
 
 
 def finish(glob, seq):
+    """Sequence losses and batch statistics from the combined exact partials.
+
+    Pinned by: test_oracle_ppo.py::test_sequence_and_batch_averages (fsum).
+    """
     S = seq.shape[0]
     seq_loss = np.array([float(int(seq[q, 0])) * 2.0 ** -52 for q in range(S)])
     n_seq_contrib = int(sum(1 for q in range(S) if int(seq[q, 1]) > 0))
@@ -120,12 +139,19 @@ def finish(glob, seq):
 
 
 def ppo(lp_cur, lp_old, adv, cu_seqlens, cfg: PPOCfg, coeff=None, resp_mask=None):
+    """Single-shard end-to-end oracle.
+
+    Pinned by: every test in test_oracle_ppo.py.
+    """
     tokens, glob, seq = local(lp_cur, lp_old, adv, cu_seqlens, cfg, coeff, resp_mask, 0)
     seq_loss, st = finish(glob, seq)
     return {**tokens, "seq_loss": seq_loss, "stats": st, "hist": glob["hist"], "seq_partials": seq}
 
 
 def clip_bounds(eps: float) -> tuple[float, float]:
-    """Paper's symmetric clip range (eq:ppo_loss): (1 - eps, 1 + eps) in binary64."""
+    """Paper's symmetric clip range (eq:ppo_loss): (1 - eps, 1 + eps) in binary64.
+
+    Pinned by: test_oracle_ppo.py::test_clip_branches_closed_form.
+    """
     return 1.0 - eps, 1.0 + eps
 

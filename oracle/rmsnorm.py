@@ -15,7 +15,10 @@ from .logprob import _as_f64
 
 
 def to_bf16(x) -> np.ndarray:
-    """Round float64 values to the nearest bf16 (ties to even); returned as float64."""
+    """Round float64 values to the nearest bf16 (ties to even); returned as float64.
+
+    Pinned by: test_oracle_rmsnorm.py::test_bf16_rounding_matches_torch_for_fp32_values.
+    """
     x = np.asarray(x, dtype=np.float64)
     m, e = np.frexp(x)                      # x = m 2^e, 0.5 <= |m| < 1
     r = np.ldexp(np.rint(np.ldexp(m, 8)), e - 8)
@@ -23,6 +26,11 @@ def to_bf16(x) -> np.ndarray:
 
 
 def rmsnorm(h, gamma, eps: float):
+    """HF RMSNorm in fp64 with the model's two bf16 roundings.
+
+    Pinned by: test_oracle_rmsnorm.py::test_spec_example_3_4 (SPEC.md S:77 worked example),
+    ::test_zero_row_and_scale_invariance.
+    """
     h64 = _as_f64(h)
     g64 = _as_f64(gamma)
     var = (h64 * h64).mean(axis=1)

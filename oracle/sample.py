@@ -25,7 +25,9 @@ MASK32 = np.uint64(0xFFFFFFFF)
 
 
 def philox4x32_10(c0, c1, c2, c3, k0, k1):
-    """Philox4x32 with 10 rounds on uint32 arrays (broadcasting); returns 4 uint32 arrays."""
+    """Philox4x32 with 10 rounds on uint32 arrays (broadcasting); returns 4 uint32 arrays.
+
+    Pinned by: test_oracle_sample.py::test_philox_known_answer_vectors (Random123 KATs)."""
     c0, c1, c2, c3 = (np.asarray(x, dtype=np.uint32) for x in (c0, c1, c2, c3))
     k0 = np.asarray(k0, dtype=np.uint32)
     k1 = np.asarray(k1, dtype=np.uint32)
@@ -43,7 +45,9 @@ def philox4x32_10(c0, c1, c2, c3, k0, k1):
 
 
 def uniforms(seed: int, row_key: int, vocab: int) -> np.ndarray:
-    """u_v for v in [0, vocab) of one row (float64 holding the exact fp32 value)."""
+    """u_v for v in [0, vocab) of one row (float64 holding the exact fp32 value).
+
+    Pinned by: test_oracle_sample.py::test_uniforms_open_interval_and_fp32_exact, ::test_sample_scores_equal_mpmath_tempered_logits_plus_gumbel."""
     nblk = (vocab + 3) // 4
     blk = np.arange(nblk, dtype=np.uint32)
     k0, k1 = np.uint32(seed & 0xFFFFFFFF), np.uint32((seed >> 32) & 0xFFFFFFFF)
@@ -54,7 +58,9 @@ def uniforms(seed: int, row_key: int, vocab: int) -> np.ndarray:
 
 
 def sample(H, W, row_keys, seed: int, temperature: float = 1.0, temperatures=None):
-    """Gumbel-max samples in fp64: returns (ids, scores [N, V]) with scores = x + g (nats)."""
+    """Gumbel-max samples in fp64: returns (ids, scores [N, V]) with scores = x + g (nats).
+
+    Pinned by: test_oracle_sample.py::test_sample_at_T07_realises_tempered_softmax_and_rejects_wrong_T (chi-square vs the mpmath tempered softmax, with power against T = 1 / 1.4 / 0.35), ::test_sample_scores_equal_mpmath_tempered_logits_plus_gumbel, ::test_sample_T_to_zero_is_argmax, ::test_sample_power_of_two_temperature_and_per_token_T."""
     H64 = _as_f64(H)
     W64 = _as_f64(W)
     N = H64.shape[0]
@@ -69,7 +75,9 @@ def sample(H, W, row_keys, seed: int, temperature: float = 1.0, temperatures=Non
 
 
 def gumbel_argmax(x, seed: int, row_key: int):
-    """argmax_v (x_v - ln(-ln u_v)) for one row of tempered logits x (nats)."""
+    """argmax_v (x_v - ln(-ln u_v)) for one row of tempered logits x (nats).
+
+    Pinned by: test_oracle_sample.py::test_gumbel_max_realises_softmax (chi-square), ::test_dominant_logit_always_wins_and_seed_changes_draws."""
     u = uniforms(seed, row_key, x.shape[0])
     s = np.asarray(x, dtype=np.float64) - np.log(-np.log(u))
     return int(np.argmax(s)), s   # first maximum = lowest column

@@ -276,3 +276,26 @@ def test_contract_decisions_match_exact_real_decisions():
             with mp.workdps(40):
                 Sx = mp.fsum(exact.k3_mp(float(x)) for x in d[cu[s]:cu[s + 1]])
             assert int(Sx <= mp.mpf(tau)) == res["seq_keep"][s]
+
+
+def test_tokens_outside_the_sequences_are_a_data_error():
+    """Reading U13b: a shard reaching past cu[S] (or starting before cu[0]) is a data error with
+    the first offending global index, never a silent attribution to some sequence."""
+    num = np.zeros(8, np.float32)
+    den = np.zeros(8, np.float32)
+    cfg = _cfg(seq_rs=oc.SEQ_K3)
+    # local tokens 100..107 against sequences covering [0, 104)
+    with pytest.raises(oc.DataError) as e:
+        oc.local_partials(num, den, [0, 50, 104], cfg, None, 100)
+    assert e.value.index == 104
+    # a shard entirely past the end: its first token
+    with pytest.raises(oc.DataError) as e:
+        oc.local_partials(num, den, [0, 50, 104], cfg, None, 200)
+    assert e.value.index == 200
+    # an earlier non-finite token wins (min index)
+    num[1] = np.nan
+    with pytest.raises(oc.DataError) as e:
+        oc.local_partials(num, den, [0, 50, 104], cfg, None, 100)
+    assert e.value.index == 101
+    # exactly covering shard: fine
+    oc.local_partials(np.zeros(4, np.float32), np.zeros(4, np.float32), [0, 50, 104], cfg, None, 100)

@@ -137,3 +137,21 @@ def test_permuting_vocab_rows_with_ids_is_invariant():
     lp, ent = logprob_entropy(H, W, ids)
     lp2, ent2 = logprob_entropy(H, W[torch.as_tensor(perm)], inv[ids])
     assert np.allclose(lp, lp2, atol=1e-12, rtol=0) and np.allclose(ent, ent2, atol=1e-12, rtol=0)
+
+
+def test_logits_equal_mpmath_dot_products_at_temperature():
+    """oracle.logprob.logits: x = H W^T / T against 40-digit dot products (§2 P:94 the
+    head's logits; reading U7 for T).  A transposed operand, a dropped or inverted T fails."""
+    import mpmath as mp
+    from oracle.logprob import logits
+    H = _rand((4, 48), 21)
+    W = _rand((7, 48), 22, 0.3)
+    for T in (0.7, 1.0, 2.5):
+        x = logits(H, W, T)
+        assert x.shape == (4, 7)
+        with mp.workdps(40):
+            for t in range(4):
+                for v in range(7):
+                    z = mp.fsum(mp.mpf(float(a)) * mp.mpf(float(b)) for a, b in zip(H[t].double(), W[v].double()))
+                    ref = float(z / mp.mpf(T))
+                    assert abs(x[t, v] - ref) <= 4 * math.ulp(abs(ref)) + 1e-300, (T, t, v)

@@ -144,3 +144,26 @@ def test_sharding_is_exact():
         seq_loss, st = op.finish(glob, seq)
         assert np.array_equal(seq_loss, full["seq_loss"]) and st == full["stats"]
         assert np.array_equal(glob["hist"], full["hist"])
+
+
+def test_non_finite_advantage_is_a_data_error():
+    """Reading U13 for NEXT-2: a non-finite advantage (GRPO whitening of a zero-variance group
+    gives NaN) or coefficient is a data error with the first index, not a histogrammed token."""
+    cu = np.array([0, 6])
+    cur = np.full(6, -1.0, np.float32)
+    old = np.full(6, -1.0, np.float32)
+    adv = np.ones(6, np.float32)
+    adv[4] = np.nan
+    with pytest.raises(op.DataError) as e:
+        op.ppo(cur, old, adv, cu, CFG)
+    assert e.value.index == 4
+    adv[4] = 1.0
+    coeff = np.ones(6, np.float32)
+    coeff[2] = np.inf
+    with pytest.raises(op.DataError) as e:
+        op.ppo(cur, old, adv, cu, CFG, coeff=coeff)
+    assert e.value.index == 2
+    adv[3] = -np.inf
+    with pytest.raises(op.DataError) as e:
+        op.local(cur, old, adv, cu, CFG, tok_begin=0)
+    assert e.value.index == 3
