@@ -1,13 +1,15 @@
 """bench.py -- throughput of the batch-invariant log-prob + TIS/RS hot path on B200.
 
-    python bench.py [--gpus N --steps K --warmup W --config c1 --impl ours|reference]
+    python bench.py [--gpus N --steps K --warmup W --config c2 --scaling strong --impl ours|reference]
     torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
 
 One step = one pass of the whole hot path over one batch:
 tim_logprob (lm_head GEMM + fused online log-softmax / gather / entropy + slice merge) on the
 rank's tokens, then tim_correct (delta, TIS, sequence-RS K3 with the paper's tau values,
-statistics; NCCL all-gather of exact partials when N > 1).  Weak scaling: every rank scores
-its own C1-shaped batch (64 sequences x 4096 tokens); value = all ranks' tokens / max-rank time.
+statistics; NCCL all-gather of exact partials when N > 1).  Default workload: C2 (Qwen3-8B head,
+d = 4096, 256 x 8192 tokens), the largest single-GPU config of BASELINE.json; C1 and C3 are
+reported as extra keys at N = 1.  Strong scaling (default): the config's global batch is cut
+into N token shards (cuts inside sequences); value = global tokens / max-rank time.
 
 Metric (BASELINE.json): logprob tokens/sec at V = 151936; also max |dlogp| across batch shapes.
 Inputs are synthetic (synth/), resident in HBM for `value`; `e2e` re-times the step through the
@@ -107,13 +109,15 @@ class ClockSampler:
 
 
 def _ncu_tensor_pct(config: str):
-    """ncu tensor-pipe activity of the logprob kernel (committed --set full summary; C1 only)."""
-    if config != "c1":
-        return None
+    """ncu tensor-pipe activity of the logprob kernel on this config, from the committed --set full
+    summary (None when no capture of this config is committed)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_logprob_summary.json")) as f:
-            m = json.load(f)["metrics"]
-        return float(m["sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"][0])
+            d = json.load(f)
+        v = d.get(f"tensor_pipe_pct_{config}")
+        if v is None and config == "c1":
+            v = d["metrics"]["sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"][0]
+        return None if v is None else float(v)
     except Exception:
         return None
 
@@ -142,12 +146,31 @@ def _hbm_traffic(key: str, n: int):
         return None
 
 
-def build_workload(cfg, rank, device):
-    seed = cfg.seed + 1000 * rank
+def build_workload(cfg, scaling, world, rank, device):
+    """The rank's slice of the workload.
+
+    strong: the config's global batch (n_seq x seq_len tokens) is cut into P token shards
+            (tim.shard_range: floor(r N / P) rounded to 256 rows, cuts inside sequences -- the
+            sequences straddle ranks); rows are drawn chunk-wise (synth.global_rows)
+            so every partition sees the same global batch.  P = 1 is the whole config.
+    weak:   every rank scores its own config-sized batch (sequences rank*S .. (rank+1)*S - 1).
+    Returns (W, H, ids, tok_begin, cu_global, resp_mask_local, n_global)."""
+    from paper_2605_14220_b200 import tim
+
     W = synth.head_weight(cfg.vocab, cfg.hidden, cfg.seed, device=device)  # replicated lm_head
+    if scaling == "strong":
+        n_glob = cfg.n_tok
+        a, b = tim.shard_range(n_glob, world, rank)
+        H, ids = synth.global_rows(n_glob, cfg.hidden, cfg.vocab, cfg.seed, a, b, W, device=device)
+        cu = synth.cu_seqlens(cfg.n_seq, cfg.seq_len)
+        mask = synth.resp_mask(cu, cfg.prompt_len)[a:b]
+        return W, H, ids, a, cu.to(device), mask.to(device), n_glob
+    seed = cfg.seed + 1000 * rank
     ids = synth.token_ids(cfg.n_tok, cfg.vocab, seed, device=device)
     H = synth.hidden_states(cfg.n_tok, cfg.hidden, seed, device=device, weight=W, ids=ids, mode="peaked")
-    return W, H, ids
+    cu = synth.cu_seqlens(cfg.n_seq * world, cfg.seq_len)
+    mask = synth.resp_mask(synth.cu_seqlens(cfg.n_seq, cfg.seq_len), cfg.prompt_len)
+    return W, H, ids, rank * cfg.n_tok, cu.to(device), mask.to(device), world * cfg.n_tok
 
 
 def run_ours(args):
@@ -168,6 +191,7 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
+    comm = tim.Comm() if world > 1 else None
     # the HBM-bound kernels are timed alone, first (before the long tensor-bound steps heat the
     # GPU into its power-capped state), against the burst copy bandwidth
     hbm_lines = {}
@@ -180,19 +204,39 @@ def run_ours(args):
     if args.n_seq:
         import dataclasses
         cfg = dataclasses.replace(cfg, n_seq=args.n_seq)
-    W, H, ids = build_workload(cfg, rank, dev)
-    N = cfg.n_tok
-    S_local = cfg.n_seq
-    # global sequence offsets: every rank owns S_local whole sequences of the global batch
-    cu = synth.cu_seqlens(S_local * world, cfg.seq_len).to(dev)
-    mask = synth.resp_mask(synth.cu_seqlens(S_local, cfg.seq_len), cfg.prompt_len).to(dev)
-    tok_begin = rank * N
-    comm = tim.Comm() if world > 1 else None
+    out = measure(tim, cfg, args, world, rank, local, dev, comm, args.steps, args.warmup, full=True)
+    out.update(hbm_lines)
+    # the other single-GPU configs of BASELINE.json as extra keys (N = 1): each its own step
+    # timing and roofline; the headline stays the config named in config.workload
+    if world == 1 and args.extra_configs:
+        extra = {}
+        for name, steps in (("c1", 5), ("c3", 2)):
+            if name == cfg.name:
+                continue
+            torch.cuda.empty_cache()
+            e = measure(tim, synth.CONFIGS[name], args, world, rank, local, dev, comm, steps, 3, full=False)
+            extra[name] = {k: e[k] for k in ("value", "unit", "ms_per_step", "steps", "warmup", "config", "roofline",
+                                             "clocks", "max_abs_dlogp_across_shapes", "correction_stats",
+                                             "scaling")}
+        out["extra_configs"] = extra
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def measure(tim, cfg, args, world, rank, local, dev, comm, steps, warmup, full):
+    scaling = args.scaling
+    W, H, ids, tok_begin, cu, mask, n_glob = build_workload(cfg, scaling, world, rank, dev)
+    N = H.shape[0]
     ccfg = tim.PRESETS["tis-srs-k3-corr-ratio"]
 
     # rollout-side log-probs: the same head with a P3 perturbation (setup, untimed)
     lp0, _ = tim.logprob(H, W, ids)
     lp_roll = synth.perturb_laplace_mix(lp0, cfg.seed + rank)
+    del lp0
     lp = torch.empty(N, dtype=torch.float32, device=dev)
     ent = torch.empty(N, dtype=torch.float32, device=dev)
     S_glob = cu.numel() - 1
@@ -203,17 +247,19 @@ def run_ours(args):
             "seq_score": torch.empty(S_glob, dtype=torch.float64, device=dev),
             "stats_raw": torch.zeros(tim.STATS_BYTES, dtype=torch.uint8, device=dev)}
     status = tim.new_status(dev)
+    # the logprob kernels run on the caller's current stream: time them with events on that stream
+    cur = torch.cuda.current_stream(dev)
 
     def step(ev=None):
         if ev is not None:
-            ev[0].record()
+            ev[0].record(cur)
         tim.logprob(H, W, ids, out=(lp, ent), status=status)
         if ev is not None:
-            ev[1].record()
+            ev[1].record(cur)
         tim.correct(lp, lp_roll, cu, ccfg, mask, tok_begin=tok_begin, comm=comm, status=status,
                     return_stats=False, out=cout)
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize()
     if world > 1:
@@ -223,18 +269,18 @@ def run_ours(args):
     clocks.start()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    t0.record()
-    for k in range(args.steps):
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    t0.record(cur)
+    for k in range(steps):
         step(evs[k])
-    t1.record()
+    t1.record(cur)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     clk = clocks.stop()
     ms = t0.elapsed_time(t1)
-    lp_ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    lp_ms = sum(a.elapsed_time(b) for a, b in evs) / steps
     if world > 1:
         t = torch.tensor([ms, lp_ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -243,7 +289,7 @@ def run_ours(args):
     assert code == 0, f"device status {code} at {first}"
     stats = tim.stats_from_bytes(cout["stats_raw"])
 
-    # invariance (untimed): a sample of rows re-scored alone and in other pack sizes, bitwise
+    # invariance (untimed): a sample of rows re-scored alone and in another pack size, bitwise
     samp = torch.arange(0, N, max(1, N // 64), device=dev)[:64]
     ref_bits = lp[samp].view(torch.int32)
     max_shape_diff = 0.0
@@ -254,6 +300,54 @@ def run_ours(args):
     if not torch.equal(a.view(torch.int32), ref_bits):
         max_shape_diff = max(max_shape_diff, (a - lp[samp]).abs().max().item())
 
+    peaks, peak_src = _peaks()
+    flop = 2.0 * cfg.vocab * cfg.hidden * N
+    achieved = flop / (lp_ms / 1e3) / 1e12
+    peak = float(peaks["bf16_tflops_sustained"])
+    value = (n_glob if scaling == "strong" else world * N) * steps / (ms / 1e3)
+    if scaling == "strong":
+        par = f"dp{world} (global batch token-sharded, cuts inside sequences)"
+        wl = (f"{cfg.name}: Qwen3-shaped lm_head d={cfg.hidden}, V={cfg.vocab}, global batch {cfg.n_seq} seqs x "
+              f"{cfg.seq_len} tokens over {world} GPU(s); logprob + entropy + tis-srs-k3-corr-ratio correction")
+    else:
+        par = f"dp{world} (token-sharded, a config-sized batch per GPU)"
+        wl = (f"{cfg.name}: Qwen3-shaped lm_head d={cfg.hidden}, V={cfg.vocab}, {cfg.n_seq} seqs x "
+              f"{cfg.seq_len} tokens per GPU; logprob + entropy + tis-srs-k3-corr-ratio correction")
+    out = {
+        "metric": "logprob tokens/sec at V=151936 (1/2/4/8 B200); max |dlogp| across batch shapes",
+        "value": value,
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": steps,
+        "warmup": warmup,
+        "ms_per_step": ms / steps,
+        "higher_is_better": True,
+        "scaling": scaling,
+        "vs_baseline": None,
+        "dtype": "bf16 inputs, fp32 tensor-core accumulate (tcgen05 kind::f16); fp64 correction",
+        "data": "synthetic (synth/: peaked-mode hidden states, N(0,0.02^2) head, seeded)",
+        "config": {
+            "workload": wl, "hidden": cfg.hidden, "vocab": cfg.vocab, "n_seq": cfg.n_seq, "seq_len": cfg.seq_len,
+            "tokens_this_gpu": N, "global_batch_tokens": n_glob, "parallelism": par,
+            "l2": "inputs larger than L2 (H %.2f GB/GPU, W %.2f GB): no flush needed" % (N * cfg.hidden * 2 / 1e9,
+                                                                                      W.numel() * 2 / 1e9),
+        },
+        "max_abs_dlogp_across_shapes": max_shape_diff,
+        "gpu_launches": KERNELS_PER_STEP * steps,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "frac_of_burst": achieved / float(peaks["bf16_tflops"]),
+                     "peak_source": peak_src + " bf16_tflops_sustained", "traffic": _traffic(cfg.name),
+                     "ncu_tensor_pipe_pct": _ncu_tensor_pct(cfg.name),
+                     "kernel": "tim_logprob (tcgen05 GEMM + fused epilogue + slice merge)",
+                     "kernel_ms": lp_ms, "algorithmic_flop_per_token": 2 * cfg.vocab * cfg.hidden,
+                     "tokens_per_launch": N},
+        "clocks": clk,
+        "correction_stats": {k: stats[k] for k in ("n_resp_tok", "n_truncated", "n_seq_rejected", "max_abs_delta",
+                                                     "mean_abs_delta", "mean_k3")},
+    }
+    if not full:
+        return out
+
     # small-batch latency (rollout-side scoring): one call on the first n rows, n <= one M-tile
     small = {}
     for n_small in (1, 64, 256):
@@ -263,75 +357,45 @@ def run_ours(args):
             tim.logprob(H[:n_small], W, ids[:n_small], out=(lps, ens))
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
+        e0.record(cur)
         for _ in range(10):
             tim.logprob(H[:n_small], W, ids[:n_small], out=(lps, ens))
-        e1.record()
+        e1.record(cur)
         torch.cuda.synchronize()
         small[str(n_small)] = round(e0.elapsed_time(e1) / 10, 4)
         assert torch.equal(lps.view(torch.int32), lp[:n_small].view(torch.int32))  # batch invariance
+    out["small_batch_latency_ms"] = {"n_tok": small, "note": "tim_logprob on the first n rows of the batch, "
+                                     "bitwise equal to their logp in the full batch"}
 
     # NEXT-1 rollout-side twin on the same batch: draw throughput and the zero-mismatch check
-    sample_info = None
     if args.sample_bench:
         keys = (torch.arange(N, device=dev, dtype=torch.int64) << 32) | rank
         for _ in range(2):
             sid, slp, sent = tim.sample(H, W, keys, seed=20260001)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
+        e0.record(cur)
         for _ in range(3):
             sid, slp, sent = tim.sample(H, W, keys, seed=20260001)
-        e1.record()
+        e1.record(cur)
         torch.cuda.synchronize()
         sms = e0.elapsed_time(e1) / 3
         rlp, rent = tim.logprob(H, W, sid)
         same = bool(torch.equal(rlp.view(torch.int32), slp.view(torch.int32)) and
                     torch.equal(rent.view(torch.int32), sent.view(torch.int32)))
-        sample_info = {"tokens_per_s": N / (sms / 1e3), "ms": sms,
-                       "tflops": 2.0 * cfg.vocab * cfg.hidden * N / (sms / 1e3) / 1e12,
-                       "logp_bitwise_equal_to_logprob": same,
-                       "kernel": "tim_sample (tcgen05 GEMM + online LSE + Philox Gumbel-max epilogue)"}
+        out["sample_twin"] = {"tokens_per_s": N / (sms / 1e3), "ms": sms,
+                              "tflops": 2.0 * cfg.vocab * cfg.hidden * N / (sms / 1e3) / 1e12,
+                              "logp_bitwise_equal_to_logprob": same,
+                              "kernel": "tim_sample (tcgen05 GEMM + online LSE + Philox Gumbel-max epilogue)"}
+        del sid, slp, sent, rlp, rent, keys
+        torch.cuda.empty_cache()
 
     # NEXT-3 head backward on one token block of the batch (dL/dlogp = 1, dL/dH = 0.01)
-    bwd_info = None
     if args.backward_bench:
-        nb = min(N, 14080)
-        gl = torch.ones(nb, device=dev)
-        ge = torch.full((nb,), 0.01, device=dev)
-        for _ in range(2):
-            dh, dw = tim.head_backward(H[:nb], W, ids[:nb], gl, ge)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(3):
-            dh, dw = tim.head_backward(H[:nb], W, ids[:nb], gl, ge)
-        e1.record()
-        torch.cuda.synchronize()
-        bms = e0.elapsed_time(e1) / 3
-        # the trainer-side variant: entropy / lse2 saved by the forward (tim_logprob_saved)
-        _, sent, slse2 = tim.logprob_saved(H[:nb], W, ids[:nb])
-        for _ in range(2):
-            dh, dw = tim.head_backward(H[:nb], W, ids[:nb], gl, ge, saved=(sent, slse2))
-        e0.record()
-        for _ in range(3):
-            dh, dw = tim.head_backward(H[:nb], W, ids[:nb], gl, ge, saved=(sent, slse2))
-        e1.record()
-        torch.cuda.synchronize()
-        sbms = e0.elapsed_time(e1) / 3
-        bwd_info = {"tokens": nb, "ms": bms, "tokens_per_s": nb / (bms / 1e3),
-                    "tflops_effective": 4 * 2.0 * cfg.vocab * cfg.hidden * nb / (bms / 1e3) / 1e12,
-                    "note": "4 passes of 2 V d flop per token: forward, gradient epilogue (logits recomputed), "
-                            "dH = G W and dW = G^T H (cuBLAS)",
-                    "kernel": "tim_head_backward",
-                    "saved": {"ms": sbms, "tokens_per_s": nb / (sbms / 1e3),
-                              "tflops_effective": 3 * 2.0 * cfg.vocab * cfg.hidden * nb / (sbms / 1e3) / 1e12,
-                              "kernel": "tim_head_backward_saved (forward's entropy / lse2 saved: 3 passes)"}}
-        del dh, dw, sent, slse2
+        out["head_backward"] = backward_bench(tim, cfg, H, W, ids, dev, cur)
         torch.cuda.empty_cache()
 
     # end to end through the public API from pinned host buffers
-    e2e = None
     Hh = H.cpu().pin_memory()
     if args.e2e_steps > 0:
         idsh = ids.cpu().pin_memory()
@@ -352,10 +416,10 @@ def run_ours(args):
             torch.distributed.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
+        e0.record(cur)
         for _ in range(args.e2e_steps):
             lph, enth, res = e2e_step()
-        e1.record()
+        e1.record(cur)
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
         if world > 1:
@@ -364,63 +428,48 @@ def run_ours(args):
             ems = t.item()
         h2d = Hh.numel() * 2 + idsh.numel() * 8 + 2 * N * 4 + maskh.numel() + cuh.numel() * 8
         d2h = 2 * N * 4 + N * 4 + N + S_glob + N * 4 + S_glob * 8 + tim.STATS_BYTES
-        e2e = {"value": world * N * args.e2e_steps / (ems / 1e3), "unit": "tokens/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-               "ms_per_step": ems / args.e2e_steps}
-
-    peaks, peak_src = _peaks()
-    flop = 2.0 * cfg.vocab * cfg.hidden * N
-    achieved = flop / (lp_ms / 1e3) / 1e12
-    peak = float(peaks["bf16_tflops_sustained"])
-    out = {
-        "metric": "logprob tokens/sec at V=151936 (1/2/4/8 B200); max |dlogp| across batch shapes",
-        "value": world * N * args.steps / (ms / 1e3),
-        "unit": "tokens/s",
-        "n_gpus": world,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": ms / args.steps,
-        "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": None,
-        "dtype": "bf16 inputs, fp32 tensor-core accumulate (tcgen05 kind::f16); fp64 correction",
-        "data": "synthetic (synth/: peaked-mode hidden states, N(0,0.02^2) head, seeded)",
-        "config": {
-            "workload": f"{cfg.name}: Qwen3-shaped lm_head d={cfg.hidden}, V={cfg.vocab}, {cfg.n_seq} seqs x "
-                        f"{cfg.seq_len} tokens per GPU; logprob + entropy + tis-srs-k3-corr-ratio correction",
-            "hidden": cfg.hidden, "vocab": cfg.vocab, "n_seq_per_gpu": cfg.n_seq, "seq_len": cfg.seq_len,
-            "tokens_per_gpu": N, "global_batch_tokens": world * N, "parallelism": f"dp{world} (token-sharded)",
-            "l2": "inputs larger than L2 (H %.2f GB/GPU, W %.2f GB)" % (H_bytes(cfg) / 1e9, W.numel() * 2 / 1e9),
-        },
-        "max_abs_dlogp_across_shapes": max_shape_diff,
-        "small_batch_latency_ms": {"n_tok": small, "note": "tim_logprob on the first n rows of the batch, "
-                                   "bitwise equal to their logp in the full batch"},
-        "gpu_launches": KERNELS_PER_STEP * args.steps,
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "frac_of_burst": achieved / float(peaks["bf16_tflops"]),
-                     "peak_source": peak_src + " bf16_tflops_sustained", "traffic": _traffic(cfg.name),
-                     "ncu_tensor_pipe_pct": _ncu_tensor_pct(cfg.name),
-                     "kernel": "tim_logprob (tcgen05 GEMM + fused epilogue + slice merge)",
-                     "kernel_ms": lp_ms, "algorithmic_flop_per_token": 2 * cfg.vocab * cfg.hidden},
-        "clocks": clk,
-        "e2e": e2e,
-        "correction_stats": {k: stats[k] for k in ("n_resp_tok", "n_truncated", "n_seq_rejected", "max_abs_delta",
-                                                     "mean_abs_delta", "mean_k3")},
-    }
-    if sample_info is not None:
-        out["sample_twin"] = sample_info
-    if bwd_info is not None:
-        out["head_backward"] = bwd_info
-    out.update(hbm_lines)
+        n_e2e = n_glob if scaling == "strong" else world * N
+        out["e2e"] = {"value": n_e2e * args.e2e_steps / (ems / 1e3), "unit": "tokens/s",
+                      "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+                      "ms_per_step": ems / args.e2e_steps}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"], out["max_abs_dlogp_vs_oracle"] = cpu_baseline(cfg, W, Hh, ids, lp, lp_roll, mask,
                                                                             args.cpu_seconds)
-    if rank == 0:
-        print(json.dumps(out), flush=True)
-    if comm is not None:
-        comm.close()
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    return out
+
+
+def backward_bench(tim, cfg, H, W, ids, dev, cur):
+    nb = min(H.shape[0], 14080)
+    gl = torch.ones(nb, device=dev)
+    ge = torch.full((nb,), 0.01, device=dev)
+    for _ in range(2):
+        dh, dw = tim.head_backward(H[:nb], W, ids[:nb], gl, ge)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(cur)
+    for _ in range(3):
+        dh, dw = tim.head_backward(H[:nb], W, ids[:nb], gl, ge)
+    e1.record(cur)
+    torch.cuda.synchronize()
+    bms = e0.elapsed_time(e1) / 3
+    # the trainer-side variant: entropy / lse2 saved by the forward (tim_logprob_saved)
+    _, sent, slse2 = tim.logprob_saved(H[:nb], W, ids[:nb])
+    for _ in range(2):
+        dh, dw = tim.head_backward(H[:nb], W, ids[:nb], gl, ge, saved=(sent, slse2))
+    e0.record(cur)
+    for _ in range(3):
+        dh, dw = tim.head_backward(H[:nb], W, ids[:nb], gl, ge, saved=(sent, slse2))
+    e1.record(cur)
+    torch.cuda.synchronize()
+    sbms = e0.elapsed_time(e1) / 3
+    return {"tokens": nb, "ms": bms, "tokens_per_s": nb / (bms / 1e3),
+            "tflops_effective": 4 * 2.0 * cfg.vocab * cfg.hidden * nb / (bms / 1e3) / 1e12,
+            "note": "4 passes of 2 V d flop per token: forward, gradient epilogue (logits recomputed), "
+                    "dH = G W and dW = G^T H (hand-written tcgen05 GEMMs, csrc/gemm.cu)",
+            "kernel": "tim_head_backward",
+            "saved": {"ms": sbms, "tokens_per_s": nb / (sbms / 1e3),
+                      "tflops_effective": 3 * 2.0 * cfg.vocab * cfg.hidden * nb / (sbms / 1e3) / 1e12,
+                      "kernel": "tim_head_backward_saved (forward's entropy / lse2 saved: 3 passes)"}}
 
 
 def H_bytes(cfg):
@@ -598,7 +647,13 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c1", choices=["c1", "c2", "c3", "toy"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "toy"],
+                    help="BASELINE.json config; default c2, the largest single-GPU config")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's global batch sharded over the GPUs (default); weak: a "
+                         "config-sized batch per GPU")
+    ap.add_argument("--no-extra-configs", dest="extra_configs", action="store_false",
+                    help="N = 1: skip the c1 / c3 extra lines")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)

@@ -150,6 +150,10 @@ tim_status tim_sample(const void* hidden_bf16, int64_t ld_hidden,
  *                       Sequences may straddle ranks.
  *   resp_mask_or_null   [n_tok_local] u8 (1 = response token); NULL = all response (U11).
  * Only response tokens enter K sums, T_s and statistics; non-response tokens get coeff 0.
+ * The shard must lie inside the sequences: cu[0] <= tok_begin and tok_begin + n_tok_local <=
+ * cu[n_seq].  cu is device memory, so this is checked on the device: a violation is a data error
+ * (device status TIM_ERR_DATA, first_bad_index = the first global token outside; reading U13b)
+ * and no access leaves the arrays.  cu must be non-decreasing (not checked; the walk is bounded). 
  * Alignment: fp32 arrays 4-B aligned (TIM_ERR_ALIGN otherwise).  When every per-token array
  * is 16-B aligned (u8 arrays 4-B) the kernels use 16-B vector accesses; otherwise (e.g. a
  * shard cut at an arbitrary token) the same results come from the scalar path, slower.
@@ -275,6 +279,10 @@ tim_status tim_correct_finish(const void* gathered_partials, int32_t nranks,
  * (that is the full [S_v][n_tok] slice-major array) and call tim_logprob_tp_merge: logp / entropy
  * are BIT-IDENTICAL to tim_logprob on the unsharded weight, for every tp -- the cross-rank
  * log-sum-exp merge is the same fixed slice-order merge.
+ * The shard MUST be exactly W rows [begin, end) of that split (whole 256-row tiles; at V = 151936
+ * and tp = 8 rank 0 owns 18944 rows, not an even V / tp split): the C ABI cannot see the shard's
+ * extent, so a shorter shard is read out of bounds and a differently cut one gives shifted
+ * columns.  The Python binding checks the shape against tim_tp_vocab_range.
  * Workspaces: >= 1024 B each (progress counters / status).  Errors as tim_logprob; tp must divide S_v.
  * -------------------------------------------------------------------------- */
 tim_status tim_tp_vocab_range(int32_t vocab, int32_t tp, int32_t rank, int32_t* begin, int32_t* end);
@@ -394,7 +402,10 @@ tim_status tim_head_backward_saved(const void* hidden_bf16, int64_t ld_hidden, c
  * resp_mask_or_null u8 (ignored when coeff is given); loss_tok, grad_logp fp32, clipped u8
  * [n_tok_local]; seq_loss_or_null [n_seq] f64; hist_or_null [2][hist_bins + 2] int64 (slot 0 =
  * underflow, hist_bins + 1 = overflow; row 0: A > 0, row 1: A < 0); stats optional.
- * Non-finite logp -> dstatus TIM_ERR_DATA (first global index), that token's loss = NaN.
+ * Data errors (dstatus TIM_ERR_DATA, first global index; readings U13 / U13b): a non-finite
+ * logp, advantage or coeff (e.g. NaN advantages from whitening a zero-variance GRPO group) -- that
+ * token's loss = NaN, grad = 0, clipped = 0, and it enters no histogram, count or sum; a shard
+ * outside [cu[0], cu[n_seq]) as for tim_correct.
  * -------------------------------------------------------------------------- */
 typedef struct {
   double clip_lo;         /* 1 - eps  (paper eq:ppo_loss) */

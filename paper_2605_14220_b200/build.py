@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtim.so")
-SOURCES = ["api.cu", "logprob.cu", "correct.cu", "ppo.cu", "rmsnorm.cu"]
+SOURCES = ["api.cu", "logprob.cu", "gemm.cu", "correct.cu", "ppo.cu", "rmsnorm.cu"]
 HEADERS = ["ptx.cuh", "tim_internal.h", "contract.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 
 #include "../../include/tim.h"
@@ -31,18 +32,27 @@ constexpr int kMaxDev = 64;
 DevInfo g_dev[kMaxDev];
 std::mutex g_mu;
 
-// debug knobs (tim_debug.h): kernel variant and an SM cap to emulate smaller GPUs
-int g_use_pair = 1;
-int g_pad_small = 1;
-int g_max_clusters = 0;
-// tuning knobs (tim_debug.h): L2 policies of the H / W tile loads and sleeping mbarrier waits
-int g_h_policy = 3;  // H tiles: evict_last (re-read for every vocab tile of the sweep)
-int g_w_policy = 2;  // W tiles: evict_first (shared by all pairs within a few tiles, then dead)
-int g_sleep_waits = 0;  // spinning mbarrier waits: +0.7-1% on C1 / C2 / sampling vs nanosleep (profiles/r01_sleep_waits_ab.txt)
-int g_sync_slack = 4;  // pairs stay within 4 vocab tiles of each other: W window ~4 MB in L2
-int g_group = 0;       // pairs per M-tile group (0 = automatic from the L2 size)
-int g_demote = 0;      // demote finished H tiles to evict_normal (applypriority)
-int g_quad = 0;        // 2-pair clusters sharing W tiles through TMA multicast
+// Debug / tuning knobs (tim_debug.h).  None of them changes a result bit; they are atomics set by
+// the tim_debug_* calls and snapshotted ONCE at the start of every library call (Knobs), so a call
+// never sees a mix of old and new settings and the hot path reads no mutable global.
+std::atomic<int> g_use_pair{1};      // cta_group::2 kernel (the numerics contract) vs ::1 bring-up
+std::atomic<int> g_pad_small{1};     // small-batch H staging
+std::atomic<int> g_max_clusters{0};  // SM cap to emulate smaller GPUs
+std::atomic<int> g_h_policy{3};      // H tiles: evict_last (re-read for every vocab tile of the sweep)
+std::atomic<int> g_w_policy{2};      // W tiles: evict_first (shared by all pairs within a few tiles, then dead)
+std::atomic<int> g_sleep_waits{0};   // spinning mbarrier waits: +0.7-1% vs nanosleep (profiles/r01_sleep_waits_ab.txt)
+std::atomic<int> g_sync_slack{4};    // pairs stay within 4 vocab tiles of each other: W window ~4 MB in L2
+std::atomic<int> g_group{0};         // pairs per M-tile group (0 = automatic from the L2 size)
+std::atomic<int> g_demote{0};        // demote finished H tiles to evict_normal (applypriority)
+std::atomic<int> g_quad{0};          // 2-pair clusters sharing W tiles through TMA multicast
+
+struct Knobs {
+  int use_pair, pad_small, max_clusters, h_policy, w_policy, sleep_waits, sync_slack, group, demote, quad;
+};
+Knobs knobs() {
+  return Knobs{g_use_pair.load(), g_pad_small.load(), g_max_clusters.load(), g_h_policy.load(), g_w_policy.load(),
+               g_sleep_waits.load(), g_sync_slack.load(), g_group.load(), g_demote.load(), g_quad.load()};
+}
 
 tim_status device_info(DevInfo** out) {
   int dev = 0;
@@ -138,10 +148,10 @@ inline int32_t vocab_slices(int32_t vocab) {
   return nvt < kMaxSlices ? nvt : kMaxSlices;
 }
 
-int pick_group(const DevInfo* dev, bool pair, int n_slices, int64_t groups, int32_t d) {
+int pick_group(const DevInfo* dev, bool pair, int n_slices, int64_t groups, int32_t d, int forced) {
   int g = 1;
-  if (pair && g_group > 0) {
-    if (n_slices % g_group == 0 && groups >= g_group) g = g_group;
+  if (pair && forced > 0) {
+    if (n_slices % forced == 0 && groups >= forced) g = forced;
   } else if (pair) {
     const double h_tile = 256.0 * d * 2.0;
     while (g < 8 && n_slices % (g * 2) == 0 && groups >= g * 2 &&
@@ -175,6 +185,7 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
                         uint64_t seed = 0, int64_t* ids_out = nullptr, int32_t tp = 1, int32_t tp_rank = 0,
                         void* tp_partial_out = nullptr, float* lse2_out = nullptr, int64_t index_base = 0,
                         bool pad_small = true) {
+  const Knobs kn = knobs();
   const bool sample = row_keys != nullptr;
   const bool tp_mode = tp_partial_out != nullptr;  // vocab-parallel rank: partials only, no merge
   if (!weight) return TIM_ERR_NULL;
@@ -189,7 +200,7 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   if (!aligned(hidden, 16)) return TIM_ERR_ALIGN;
   if (!ws) return TIM_ERR_NULL;
   if (!aligned(ws, 16)) return TIM_ERR_ALIGN;
-  const bool pad = pad_small && g_pad_small && !tp_mode && small_pad_rows(n_tok) > 0;
+  const bool pad = pad_small && kn.pad_small && !tp_mode && small_pad_rows(n_tok) > 0;
   const size_t ws_need = tp_mode ? kWsHeaderBytes
                                  : (sample ? tim_sample_workspace_bytes(n_tok, d, vocab)
                                            : tim_logprob_workspace_bytes(n_tok, d, vocab)) -
@@ -207,10 +218,10 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   tim_status st = device_info(&dev);
   if (st != TIM_OK) return st;
 
-  const bool pair = g_use_pair != 0;
+  const bool pair = kn.use_pair != 0;
   // 2-pair multicast clusters when the live H tiles of all pairs fit in L2 (d <= 2048 on B200);
   // otherwise 1-pair clusters with M-tile groups (below).  Never changes a result bit.
-  const bool quad = pair && g_quad != 0 && dev->max_pair_clusters >= 2 &&
+  const bool quad = pair && kn.quad != 0 && dev->max_pair_clusters >= 2 &&
                     dev->max_pair_clusters * 256.0 * d * 2.0 <= 0.75 * dev->l2_bytes;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   uint8_t* wsb = static_cast<uint8_t*>(ws);
@@ -253,26 +264,26 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   p.w_row0 = row0;
   p.debug_logits = debug_logits;
   p.debug_ld = debug_ld;
-  p.h_policy = g_h_policy;
-  p.w_policy = g_w_policy;
-  p.sleep_waits = g_sleep_waits;
+  p.h_policy = kn.h_policy;
+  p.w_policy = kn.w_policy;
+  p.sleep_waits = kn.sleep_waits;
   p.progress = reinterpret_cast<uint32_t*>(wsb + kWsProgressOffset);
-  p.sync_slack = g_sync_slack;
+  p.sync_slack = kn.sync_slack;
   p.hidden_ptr = h_tma;
   p.ld_hidden_bytes = h_ld * 2;
-  p.demote = g_demote;
+  p.demote = kn.demote;
   p.row_keys = row_keys;
   p.seed = seed;
   p.partials2 = sample ? partials + static_cast<size_t>(vocab_slices(vocab)) * static_cast<size_t>(n_tok) : nullptr;
   const int64_t n_units = static_cast<int64_t>(quad ? (p.n_mt + 1) / 2 : p.n_mt) * p.n_slices;
   int64_t ctas_cap = quad ? dev->max_pair_clusters / 2 : (pair ? dev->max_pair_clusters : dev->max_single_ctas);
-  if (g_max_clusters > 0 && g_max_clusters < ctas_cap) ctas_cap = g_max_clusters;
+  if (kn.max_clusters > 0 && kn.max_clusters < ctas_cap) ctas_cap = kn.max_clusters;
   const int64_t groups = n_units < ctas_cap ? n_units : ctas_cap;
   const int grid = static_cast<int>(groups * (quad ? 4 : (pair ? 2 : 1)));
   // Pairs sharing an M-tile: smallest G in {1, 2, 4, 8} (dividing S_v, <= #pairs) whose live H
   // tiles (one 256-row tile per group) fit in ~75% of L2.  Performance only: which pair runs
   // which (M-tile, slice) unit never changes a row's arithmetic.
-  p.group = quad ? 1 : pick_group(dev, pair, p.n_slices, groups, d);
+  p.group = quad ? 1 : pick_group(dev, pair, p.n_slices, groups, d, kn.group);
   if (launch_logprob_fwd(pair, debug_logits != nullptr, sample, quad, th, tw, p, grid, s) != cudaSuccess)
     return TIM_ERR_CUDA;
   if (tp_mode) return TIM_OK;  // the caller all-gathers the slice partials, then tim_logprob_tp_merge
@@ -366,57 +377,6 @@ NcclApi* nccl() {
   return &api;
 }
 constexpr int kNcclInt8 = 0;
-
-// ------------------------------------------------------------------ cuBLAS --
-// The two plain GEMMs of the head backward (dH = G W, dW = G^T H) go to cuBLAS, loaded at run
-// time (libcublas.so.12, the one torch already mapped when present).  Deterministic run to run.
-typedef void* cublas_handle_t;
-typedef int (*PFN_cublasCreate)(cublas_handle_t*);
-typedef int (*PFN_cublasSetStream)(cublas_handle_t, cudaStream_t);
-typedef int (*PFN_cublasGemmEx)(cublas_handle_t, int, int, int, int, int, const void*, const void*, int, int,
-                                const void*, int, int, const void*, void*, int, int, int, int);
-struct CublasApi {
-  bool ok = false;
-  PFN_cublasCreate create = nullptr;
-  PFN_cublasSetStream set_stream = nullptr;
-  PFN_cublasGemmEx gemm_ex = nullptr;
-  cublas_handle_t handle[kMaxDev] = {};
-};
-CublasApi* cublas() {
-  static CublasApi api;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* h = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("libcublas.so", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) return;
-    api.create = reinterpret_cast<PFN_cublasCreate>(dlsym(h, "cublasCreate_v2"));
-    api.set_stream = reinterpret_cast<PFN_cublasSetStream>(dlsym(h, "cublasSetStream_v2"));
-    api.gemm_ex = reinterpret_cast<PFN_cublasGemmEx>(dlsym(h, "cublasGemmEx"));
-    api.ok = api.create && api.set_stream && api.gemm_ex;
-  });
-  return &api;
-}
-constexpr int kCublasOpN = 0, kCublasOpT = 1, kCudaR32F = 0, kCudaR16BF = 14, kCublasCompute32F = 68,
-              kCublasGemmDefault = -1;
-
-// column-major C[m x n] = alpha op(A) op(B) + beta C, bf16 inputs, fp32 accumulate / output
-tim_status gemm_bf16_f32(cudaStream_t s, int opa, int opb, int m, int n, int k, const void* A, int lda, const void* B,
-                         int ldb, float beta, float* C, int ldc) {
-  CublasApi* api = cublas();
-  if (!api->ok) return TIM_ERR_UNSUPPORTED;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev >= kMaxDev) return TIM_ERR_CUDA;
-  {
-    std::lock_guard<std::mutex> lk(g_mu);
-    if (!api->handle[dev] && api->create(&api->handle[dev]) != 0) return TIM_ERR_CUDA;
-  }
-  if (api->set_stream(api->handle[dev], s) != 0) return TIM_ERR_CUDA;
-  const float alpha = 1.0f;
-  return api->gemm_ex(api->handle[dev], opa, opb, m, n, k, &alpha, A, kCudaR16BF, lda, B, kCudaR16BF, ldb, &beta, C,
-                      kCudaR32F, ldc, kCublasCompute32F, kCublasGemmDefault) == 0
-             ? TIM_OK
-             : TIM_ERR_CUDA;
-}
 
 }  // namespace
 
@@ -835,6 +795,7 @@ static tim_status head_backward_impl(const void* hidden_bf16, int64_t ld_hidden,
                                      const float* grad_logp, const float* grad_ent_or_null,
                                      float* dhidden_or_null, float* dweight_or_null, void* ws, size_t ws_bytes,
                                      tim_device_status* dstatus, void* stream) {
+  const Knobs kn = knobs();
   const bool saved = ent_saved != nullptr;
   if (!weight_bf16) return TIM_ERR_NULL;
   if (n_tok < 0 || n_tok >= (int64_t(1) << 31)) return TIM_ERR_SHAPE;
@@ -860,7 +821,6 @@ static tim_status head_backward_impl(const void* hidden_bf16, int64_t ld_hidden,
   DevInfo* dev = nullptr;
   tim_status st = device_info(&dev);
   if (st != TIM_OK) return st;
-  if (!cublas()->ok) return TIM_ERR_UNSUPPORTED;
 
   const int64_t nb = bwd_block_rows(n_tok, vocab), g_ld = bwd_g_ld(vocab);
   uint8_t* w8 = static_cast<uint8_t*>(ws);
@@ -908,11 +868,11 @@ static tim_status head_backward_impl(const void* hidden_bf16, int64_t ld_hidden,
     p.n_vt = nvt;
     p.n_slices = S;
     p.n_slices_total = S;
-    p.h_policy = g_h_policy;
-    p.w_policy = g_w_policy;
-    p.sleep_waits = g_sleep_waits;
+    p.h_policy = kn.h_policy;
+    p.w_policy = kn.w_policy;
+    p.sleep_waits = kn.sleep_waits;
     p.progress = reinterpret_cast<uint32_t*>(fwd_ws + kWsProgressOffset);
-    p.sync_slack = g_sync_slack;
+    p.sync_slack = kn.sync_slack;
     p.hidden_ptr = hb;
     p.ld_hidden_bytes = ld_hidden * 2;
     p.grad_logp = grad_logp + b0;
@@ -924,23 +884,29 @@ static tim_status head_backward_impl(const void* hidden_bf16, int64_t ld_hidden,
     p.g_col0 = 0;
     const int64_t n_units = static_cast<int64_t>(p.n_mt) * S;
     int64_t cap = dev->max_pair_clusters;
-    if (g_max_clusters > 0 && g_max_clusters < cap) cap = g_max_clusters;
+    if (kn.max_clusters > 0 && kn.max_clusters < cap) cap = kn.max_clusters;
     const int64_t groups = n_units < cap ? n_units : cap;
-    p.group = pick_group(dev, true, S, groups, d);
+    p.group = pick_group(dev, true, S, groups, d, kn.group);
     CUtensorMap tg;
     if (!encode_g_store(&tg, G, nbc, vocab, g_ld)) return TIM_ERR_CUDA;
     if (launch_head_grad(th, tw, tg, p, static_cast<int>(groups * 2), s) != cudaSuccess) return TIM_ERR_CUDA;
-    // (3) dH[b] = G W  (column-major: dH^T[d x nbc] = W^T[d x V] G^T[V x nbc])
+    // (3) dH[b] = G W and (4) dW += G^T H[b]: the hand-written tcgen05 GEMMs (gemm.cu).  dH's K
+    //     order (ascending V in steps of 16) is a constant of (V, d): batch-invariant rows.
+    int max_pairs = dev->max_pair_clusters;
+    if (kn.max_clusters > 0 && kn.max_clusters < max_pairs) max_pairs = kn.max_clusters;
     if (dhidden_or_null) {
-      st = gemm_bf16_f32(s, kCublasOpN, kCublasOpN, d, static_cast<int>(nbc), vocab, weight_bf16, d, G,
-                         static_cast<int>(g_ld), 0.0f, dhidden_or_null + b0 * d, d);
-      if (st != TIM_OK) return st;
+      CUtensorMap ta, tb;
+      if (!encode_bf16_2d(&ta, G, nbc, vocab, g_ld, 128)) return TIM_ERR_CUDA;        // A = G, K-major
+      if (!encode_bf16_2d(&tb, weight_bf16, vocab, d, d, 64)) return TIM_ERR_CUDA;    // B = W, MN-major
+      BwdGemmParams gp{dhidden_or_null + b0 * d, d, static_cast<int>(nbc), d, vocab};
+      if (launch_bwd_gemm_dh(ta, tb, gp, max_pairs, s) != cudaSuccess) return TIM_ERR_CUDA;
     }
-    // (4) dW += G^T H[b]  (column-major: dW^T[d x V] += H^T[d x nbc] G[nbc x V])
     if (dweight_or_null) {
-      st = gemm_bf16_f32(s, kCublasOpN, kCublasOpT, d, vocab, static_cast<int>(nbc), hb,
-                         static_cast<int>(ld_hidden), G, static_cast<int>(g_ld), 1.0f, dweight_or_null, d);
-      if (st != TIM_OK) return st;
+      CUtensorMap ta, tb;
+      if (!encode_bf16_2d(&ta, G, nbc, vocab, g_ld, 64)) return TIM_ERR_CUDA;         // A = G^T, MN-major
+      if (!encode_bf16_2d(&tb, hb, nbc, d, ld_hidden, 64)) return TIM_ERR_CUDA;       // B = H, MN-major
+      BwdGemmParams gp{dweight_or_null, d, vocab, d, static_cast<int>(nbc)};
+      if (launch_bwd_gemm_dw(ta, tb, gp, max_pairs, s) != cudaSuccess) return TIM_ERR_CUDA;
     }
   }
   return TIM_OK;

@@ -161,6 +161,21 @@ __device__ __forceinline__ long long seq_of(const int64_t* cu, long long n_seq, 
   return lo;
 }
 
+// The shard [tok_begin, tok_begin + n) must lie inside the global sequences [cu[0], cu[n_seq]).
+// A token outside is a data error (reading U13b): its global index (the first one outside) goes
+// to the status through bad_inv (the max of kBadSentinel - index, i.e. the min index wins).
+__device__ __forceinline__ void shard_range_check(const int64_t* cu, long long n_seq, long long tok_begin,
+                                                  long long n, unsigned long long& bad_inv) {
+  if (n <= 0) return;
+  const long long c0 = __ldg(cu), c1 = __ldg(cu + n_seq);
+  long long first = -1;
+  if (tok_begin < c0) first = tok_begin;
+  else if (tok_begin + n > c1) first = tok_begin > c1 ? tok_begin : c1;
+  if (first >= 0) {
+    const unsigned long long b = kBadSentinel - static_cast<unsigned long long>(first);
+    bad_inv = b > bad_inv ? b : bad_inv;
+  }
+}
 
 // exact int128 -> double, round to nearest even
 __device__ __forceinline__ double i128_to_double(__int128 x) {

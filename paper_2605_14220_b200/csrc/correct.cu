@@ -231,7 +231,9 @@ __device__ __forceinline__ void chunk_body(const LocalParams& p, LaneState& st, 
       const long long g = p.tok_begin + i;
       const double d = dv[k];
       if (kSeq) {
-        while (g >= st.next_b) {  // crossed into a later sequence (skips empty ones)
+        // crossed into a later sequence (skips empty ones); bounded by the last sequence so a
+        // shard reaching past cu[n_seq] (a data error, flagged by the range check) stays in bounds
+        while (g >= st.next_b && st.sid + 1 < p.n_seq) {
           SeqAcc a;
           a.sid = st.sid;
           a.x = st.seq_x;
@@ -332,6 +334,8 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
     st.next_b = __ldg(p.cu + st.sid + 1);
     seq_lim = st.next_b - p.tok_begin - (kTpl - 1);
   }
+
+  if (blockIdx.x == 0 && threadIdx.x == 0) shard_range_check(p.cu, p.n_seq, p.tok_begin, p.n, st.bad_inv);
 
   FastAcc fa;
   fa.k1 = fa.k3 = fa.ab = fa.seq = fa.mx = 0.0;

@@ -18,6 +18,7 @@
 #include <cuda_bf16.h>
 #include <math_constants.h>
 
+#include <atomic>
 #include <cstdint>
 
 #include "ptx.cuh"
@@ -57,40 +58,44 @@ __device__ __forceinline__ float chunk_max32(const float (&y)[32]) {
 }
 
 // Online update of the row state with 32 consecutive columns (fixed order, fixed tree).
-// Log2 domain: y = z * c with c = RN(log2(e) / T) > 0.  The chunk max is taken on the raw
-// accumulators (RN is monotone, so RN(max z * c) = max RN(z * c)), and t = y - m is formed by
-// one FFMA (z * c - m rounded once): per logit FMNMX(3) + FFMA + MUFU.EX2 + FADD + FFMA.
+// Log2 domain with c = RN(log2(e) / T) > 0.  The running max is kept on the raw fp32 accumulators
+// (mz), and t = RN(RN(z - mz) c) is the column's log2 weight relative to it: the column holding
+// the max has t = 0 exactly, so its weight is ex2(0) = 1 exactly and a one-column vocabulary gives
+// logp = 0 and H = 0 exactly (reading U16).  (Subtract-then-scale cannot be contracted
+// into an FMA; ptxas does contract a packed mul.rn.f32x2 + add.rn.f32x2 pair, so y - m formed as
+// RN(z c) - m would silently become fma(z, c, -m).)  The slice partial stores m = RN(mz c), the
+// same rounding as the gathered y_a = RN(z_a c).  Per logit FMNMX(3) + FADD + FMUL + MUFU.EX2 +
+// FADD + FFMA, in packed pairs.
 template <bool kTail>
 __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float c, int col0, int vocab, int64_t a,
-                                          float& m, float& s, float& u, float& ya) {
+                                          float& mz, float& s, float& u, float& ya) {
   float z[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
     z[i] = __uint_as_float(r[i]);
     if (kTail && col0 + i >= vocab) z[i] = -CUDART_INF_F;
   }
-  const float cmax = chunk_max32(z) * c;
+  const float zmax = chunk_max32(z);
   const int64_t rel = a - col0;
   if (static_cast<uint64_t>(rel) < 32u) {
 #pragma unroll
     for (int i = 0; i < 32; ++i)
       if (rel == i) ya = z[i] * c;
   }
-  if (cmax > m) {
-    const float dm = m - cmax;  // -inf on the first chunk of a slice
+  if (zmax > mz) {
+    const float dm = __fmul_rn(__fsub_rn(mz, zmax), c);  // -inf on the first chunk of a slice
     const float sc = ex2_approx(dm);
     u = (s > 0.f) ? sc * fmaf(s, dm, u) : 0.f;
     s = s * sc;
-    m = cmax;
+    mz = zmax;
   }
-  const float nm = -m;
   // four partial sums per quantity (column i goes to i mod 4, ascending i), two at a time in
   // packed fp32 pairs: the same per-lane operations as four scalar chains
   float2 s01 = make_float2(0.f, 0.f), s23 = s01, u01 = s01, u23 = s01;
-  const float2 c2 = make_float2(c, c), nm2 = make_float2(nm, nm);
+  const float2 c2 = make_float2(c, c), nmz2 = make_float2(-mz, -mz);
 #pragma unroll
   for (int i = 0; i < 32; i += 2) {
-    float2 t = ffma2(make_float2(z[i], z[i + 1]), c2, nm2);
+    float2 t = fmul2(fadd2(make_float2(z[i], z[i + 1]), nmz2), c2);
     if (kTail) {  // masked column: e = 0, e * t = 0 (no -inf * 0)
       t.x = fmaxf(t.x, -256.f);
       t.y = fmaxf(t.y, -256.f);
@@ -487,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t a = (valid && p.ids) ? __ldg(p.ids + row) : int64_t(-1);
       const float T = (valid && p.temps) ? __ldg(p.temps + row) : p.temperature;
       const float c = __fdiv_rn(kLog2eF, T);
-      float m = -CUDART_INF_F, s = 0.f, uu = 0.f, ya = -CUDART_INF_F;
+      float m = -CUDART_INF_F, s = 0.f, uu = 0.f, ya = -CUDART_INF_F;  // m: running max of the raw z
       float gA = 0.f, gB = 0.f, gS = 0.f, lse2 = 0.f;  // gradient mode (NEXT-3): grad_chunk's row constants
       if (kGrad && valid) {
         const float gl = __ldg(p.grad_logp + row);
@@ -583,7 +588,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (acc == 0) aphase ^= 1;
       }
       if (valid && !kGrad) {
-        p.partials[static_cast<int64_t>(j) * p.n_tok + row] = make_float4(m, s, uu, ya);
+        // m = RN(mz c): the slice max in log2 units, rounded like the gathered y_a
+        p.partials[static_cast<int64_t>(j) * p.n_tok + row] = make_float4(__fmul_rn(m, c), s, uu, ya);
         if (kSample)
           p.partials2[static_cast<int64_t>(j) * p.n_tok + row] =
               make_float4(best_s, best_y, __int_as_float(best_col), 0.f);
@@ -680,11 +686,16 @@ static cudaError_t launch_fwd(const CUtensorMap& th, const CUtensorMap& tw, cons
   auto kern = logprob_fwd_kernel<kPair, kDebug, kSample, kNP, kGrad>;
   // gradient mode: + 1 KB alignment slack and 4 warps x 2 x 2 KB G staging tiles
   constexpr int kSmem = C::kSmemBytes + (kGrad ? 1024 + kEpiWarps * 4096 : 0);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  // the attribute is per device: a process driving several GPUs sets it once on each
+  static std::atomic<bool> attr_set[kMaxDevices];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  if (!attr_set[dev].load()) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set[dev].store(true);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);

@@ -109,6 +109,8 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
     next_b = __ldg(p.cu + acc.sid + 1);
   }
 
+  if (blockIdx.x == 0 && threadIdx.x == 0) shard_range_check(p.cu, p.n_seq, p.tok_begin, p.n, bad_inv);
+
   PpoChunk nxt;
   if (c_begin < c_end) nxt = ppo_load(p, c_begin * kPpoWarpTok + lane * kPpoTpl);
   for (long long ch = c_begin; ch < c_end; ++ch) {
@@ -206,7 +208,7 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
         if (i >= p.n) continue;
         const long long g = p.tok_begin + i;
         const double d = dv[k];
-        while (g >= next_b) {  // leave the sequence(s) the lane has walked past
+        while (g >= next_b && acc.sid + 1 < p.n_seq) {  // leave the sequence(s) walked past (bounded)
           flush_seq(p.seqp, acc);
           acc.x = 0;
           acc.t = 0;
@@ -214,7 +216,9 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
           acc.sid += 1;
           next_b = __ldg(p.cu + acc.sid + 1);
         }
-        if (!isfinite(d)) {
+        // data error (U13): a non-finite log-prob, advantage or weight -- loss NaN, grad 0, the
+        // token excluded from the histogram and every sum
+        if (!isfinite(d) || !isfinite(ad_[k]) || !isfinite(wv_[k])) {
           const unsigned long long b = kBadSentinel - static_cast<unsigned long long>(g);
           bad_inv = b > bad_inv ? b : bad_inv;
           l_out[k] = CUDART_NAN_F;

@@ -18,6 +18,7 @@ struct WsHeader {
 };
 static_assert(sizeof(WsHeader) == 64, "WsHeader size");
 constexpr unsigned long long kBadSentinel = 1ull << 62;
+constexpr int kMaxDevices = 64;  // devices per process the library keeps per-device state for
 constexpr size_t kWsHeaderBytes = 1024;      // WsHeader + per-pair progress counters
 constexpr size_t kWsProgressOffset = 64;
 constexpr int kMaxProgress = (kWsHeaderBytes - kWsProgressOffset) / 4;
@@ -115,6 +116,18 @@ cudaError_t launch_pad_rows(const void* src, int64_t ld_src_bytes, void* dst, in
 cudaError_t launch_head_grad(const CUtensorMap& th, const CUtensorMap& tw, const CUtensorMap& tg,
                              const LogprobParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_sample_merge(const MergeParams& p, cudaStream_t stream);
+
+// gemm.cu -- head-backward GEMMs C[m, n] (fp32, row pitch ldc) = A[m, k] B[k, n] (bf16 operands
+// through TMA tensor maps): dH stores, dW accumulates (red.global.add)
+struct BwdGemmParams {
+  float* c;
+  int64_t ldc;
+  int m, n, k;
+};
+cudaError_t launch_bwd_gemm_dh(const CUtensorMap& tg_kmajor, const CUtensorMap& tw_mn, const BwdGemmParams& p,
+                               int max_pairs, cudaStream_t stream);
+cudaError_t launch_bwd_gemm_dw(const CUtensorMap& tg_mn, const CUtensorMap& th_mn, const BwdGemmParams& p,
+                               int max_pairs, cudaStream_t stream);
 
 // correct.cu
 struct CorrectDevCfg {

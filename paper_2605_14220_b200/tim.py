@@ -155,7 +155,12 @@ _ws_cache: dict = {}
 
 
 def _workspace(device, nbytes: int, tag: str) -> torch.Tensor:
-    key = (str(device), tag)
+    """Cached workspace per (device, CURRENT STREAM, tag).  Calls on different streams never share
+    a buffer (the library's per-call header, progress counters and partials would race), and a
+    buffer is allocated on -- and, when it grows, released to the caching allocator from -- the
+    stream that uses it, so the reuse is stream-ordered."""
+    stream = torch.cuda.current_stream(device)
+    key = (str(device), stream.cuda_stream, tag)
     t = _ws_cache.get(key)
     if t is None or t.numel() < nbytes:
         t = torch.empty(max(nbytes, 256) + 256, dtype=torch.uint8, device=device)
@@ -306,6 +311,12 @@ def logprob_tp_partial(hidden: torch.Tensor, weight_shard: torch.Tensor, vocab: 
     """One rank of a vocab-parallel head: this rank's slice partials (uint8 block) -- tim_logprob_tp_partial."""
     dev = hidden.device
     N, d = hidden.shape
+    b, e = tp_vocab_range(vocab, tp, rank)
+    if hidden.dtype != torch.bfloat16 or weight_shard.dtype != torch.bfloat16:
+        raise TypeError("hidden and weight_shard must be bfloat16")
+    if weight_shard.dim() != 2 or weight_shard.shape[1] != d or weight_shard.shape[0] != e - b:
+        raise ValueError(f"weight_shard must be W[{b}:{e}] ([{e - b}, {d}]: whole 256-row slices of the fixed "
+                         f"split, tim_tp_vocab_range), got {tuple(weight_shard.shape)}")
     weight_shard = weight_shard.contiguous()
     ids = ids.to(device=dev, dtype=torch.int64).contiguous()
     if temperatures is not None:
@@ -523,14 +534,16 @@ def stats_from_bytes(raw: torch.Tensor) -> dict:
 
 
 def _prep_correct(lp_num, lp_den, cu_seqlens, resp_mask, dev):
+    """Every tensor argument is moved to `dev` (a no-op when already there): a host pointer must
+    never reach a kernel, whatever mix of host and device tensors the caller passes."""
     host = not lp_num.is_cuda
-    if host:
-        lp_num = lp_num.to(dev, non_blocking=True)
-        lp_den = lp_den.to(dev, non_blocking=True)
-        if resp_mask is not None:
-            resp_mask = resp_mask.to(dev, non_blocking=True)
-    if not cu_seqlens.is_cuda:
-        cu_seqlens = cu_seqlens.to(dev, non_blocking=True)
+    lp_num = lp_num.to(dev, non_blocking=True)
+    lp_den = lp_den.to(dev, non_blocking=True)
+    if resp_mask is not None:
+        resp_mask = resp_mask.to(dev, non_blocking=True)
+    cu_seqlens = cu_seqlens.to(dev, non_blocking=True)
+    if lp_den.numel() != lp_num.numel() or (resp_mask is not None and resp_mask.numel() != lp_num.numel()):
+        raise ValueError("lp_num, lp_den and resp_mask must have one value per token")
     lp_num = lp_num.to(torch.float32).contiguous()
     lp_den = lp_den.to(torch.float32).contiguous()
     cu_seqlens = cu_seqlens.to(torch.int64).contiguous()

@@ -107,6 +107,31 @@ def hidden_states(n: int, hidden: int, seed: int, device="cpu", weight: torch.Te
     return out
 
 
+ROW_CHUNK = 65536  # rows per independently seeded chunk of a global batch (global_rows)
+
+
+def global_rows(n_total: int, hidden: int, vocab: int, seed: int, a: int, b: int, weight: torch.Tensor,
+                device="cpu", mode: str = "peaked") -> tuple[torch.Tensor, torch.Tensor]:
+    """(H [b - a, d], ids [b - a]) = rows [a, b) of an n_total-row global batch in which every
+    ROW_CHUNK-row chunk is drawn from its own seed, so any partition of the rows over ranks (a
+    strong-scaling shard, a cut inside a sequence) reproduces exactly the same values."""
+    if not (0 <= a <= b <= n_total):
+        raise ValueError("bad row range")
+    Hs, Is = [], []
+    for c in range(a // ROW_CHUNK, (b - 1) // ROW_CHUNK + 1 if b > a else a // ROW_CHUNK):
+        lo, hi = c * ROW_CHUNK, min(n_total, (c + 1) * ROW_CHUNK)
+        sc = seed * 1009 + c
+        idc = token_ids(hi - lo, vocab, sc, device=device)
+        hc = hidden_states(hi - lo, hidden, sc, device=device, weight=weight, ids=idc, mode=mode)
+        x0, x1 = max(a, lo) - lo, min(b, hi) - lo
+        Hs.append(hc[x0:x1])
+        Is.append(idc[x0:x1])
+    if not Hs:
+        return (torch.empty(0, hidden, dtype=torch.bfloat16, device=device),
+                torch.empty(0, dtype=torch.int64, device=device))
+    return torch.cat(Hs), torch.cat(Is)
+
+
 def cu_seqlens(n_seq: int, seq_len: int, seed: int = 0, variable: bool = False, device="cpu") -> torch.Tensor:
     """int64 [S+1] prefix offsets; equal lengths, or L_s ~ U[L/8, L] when variable."""
     if variable:

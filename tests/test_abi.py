@@ -195,3 +195,21 @@ def test_debug_knobs_validate_arguments(L):
     assert L.tim_debug_set_tuning(3, 2, 0, 4) == 0          # the defaults
     assert L.tim_debug_set_kernel(2, 0) == 4 and L.tim_debug_set_kernel(1, -1) == 4
     assert L.tim_debug_set_kernel(1, 0) == 0
+
+
+def test_tp_partial_rejects_a_shard_of_the_wrong_split():
+    """a standard even vocab-parallel shard (V / tp rows) is not the fixed split of
+    whole 256-row slices; the binding rejects it before any launch (no GPU needed)."""
+    import torch
+    from paper_2605_14220_b200 import tim
+    V, tp, d = 151936, 8, 128
+    b, e = tim.tp_vocab_range(V, tp, 0)
+    assert (b, e) == (0, 18944)
+    H = torch.zeros(4, d, dtype=torch.bfloat16)
+    ids = torch.zeros(4, dtype=torch.int64)
+    with pytest.raises(ValueError):
+        tim.logprob_tp_partial(H, torch.zeros(V // tp, d, dtype=torch.bfloat16), V, tp, 0, ids)
+    with pytest.raises(ValueError):
+        tim.logprob_tp_partial(H, torch.zeros(e - b, d + 64, dtype=torch.bfloat16), V, tp, 0, ids)
+    with pytest.raises(TypeError):
+        tim.logprob_tp_partial(H, torch.zeros(e - b, d, dtype=torch.float32), V, tp, 0, ids)

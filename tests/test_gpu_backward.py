@@ -1,8 +1,14 @@
-"""GPU tests of the head backward (NEXT-3): tim_head_backward vs oracle.backward.
+"""GPU tests of the head backward (NEXT-3): tim_head_backward vs oracle.backward, ELEMENT-WISE.
 
-Tolerance (U24): the path rounds G = dL/dz to bf16 (relative error <= 2^-9 per
-element, independent across elements) and the GEMMs accumulate in fp32, so the relative
-Frobenius error of dhidden / dweight is ~2^-9 / sqrt(3) ~ 1.1e-3; the bound is 4e-3.
+Per-element bound (U24), derived from the arithmetic of the path:
+  * G = dL/dz is rounded to bf16 (relative error <= 2^-9 per element) and both GEMMs accumulate in
+    fp32 on the tensor cores in K = 16 steps; even with truncating adds that is <= (K / 16) 2^-23
+    relative to sum_k |G||B| (K = V = 151936: 1.13e-3; K = token block <= 14080: 1.0e-4), so
+    2^-9 + 1.13e-3 = 3.1e-3 < 2^-8 of  S = sum_k |G_ik| |B_kj|  (B = W for dH, H for dW);
+  * p = ex2(y - lse2) carries the fp32 logit / lse error (measured ~4e-6 relative; 1e-4 taken):
+    it enters G as (|g| + |e|) p delta / T, which the 1[v = a] term does not scale with G, so it
+    gets its own term  1e-4 (|g| + |e|) / T (P |W|)  (resp. (1e-4 (|g| + |e|) / T P)^T |H|).
+  |dH - dH_ref| <= 2^-8 |G| |W| + 1e-4 ((|g| + |e|) / T) P |W|, element by element; same for dW.
 Exact properties: zero upstream gradients give exact zeros; repeated calls are bitwise equal;
 token blocks accumulate dweight; a bad id reports its global index.
 """
@@ -12,14 +18,47 @@ import torch
 
 import synth
 from oracle.backward import grad_logits, head_backward as o_backward
+from oracle.logprob import logits as o_logits
 
 pytestmark = pytest.mark.gpu
 DEV = "cuda"
-TOL = 4e-3
+REL = 2.0 ** -8
+DP = 1e-4
 
 
 def _rel(a, ref):
     return float(np.linalg.norm(a - ref) / max(np.linalg.norm(ref), 1e-30))
+
+
+def _np(x):
+    return None if x is None else x.detach().cpu().double().numpy()
+
+
+def _bounds(H, W, ids, gl, ge, T):
+    """(G, P, dH bound, dW bound) from the fp64 oracle (G = oracle.backward.grad_logits, P from the
+    pinned oracle.logprob.logits)."""
+    Hn, Wn = _np(H), _np(W)
+    N = Hn.shape[0]
+    Tn = np.ones(N) if T is None else _np(T)
+    g = _np(gl)
+    e = np.zeros(N) if ge is None else _np(ge)
+    G = grad_logits(H.cpu(), W.cpu(), ids.cpu(), gl.cpu(), None if ge is None else ge.cpu(), 1.0,
+                    None if T is None else T.cpu())
+    x = o_logits(H.cpu(), W.cpu()) / Tn[:, None]
+    P = np.exp(x - x.max(axis=1, keepdims=True))
+    P /= P.sum(axis=1, keepdims=True)
+    c = DP * (np.abs(g) + np.abs(e)) / Tn
+    aG = np.abs(G)
+    bh = REL * (aG @ np.abs(Wn)) + c[:, None] * (P @ np.abs(Wn))
+    bw = REL * (aG.T @ np.abs(Hn)) + (c[:, None] * P).T @ np.abs(Hn)
+    return G, bh, bw
+
+
+def _assert_within(got, ref, bound, what):
+    err = np.abs(got - ref)
+    worst = float((err / np.maximum(bound, 1e-300)).max())
+    assert np.all(err <= bound), (what, worst)
+    return worst
 
 
 def _problem(N, d, V, seed, mode="flat"):
@@ -40,31 +79,32 @@ def _problem(N, d, V, seed, mode="flat"):
 ])
 def test_backward_matches_oracle(tim, N, d, V, mode, ent, temps):
     H, W, ids, gl, ge, T = _problem(N, d, V, N + V, mode)
-    dh, dw = tim.head_backward(H, W, ids, gl, ge if ent else None, 1.0, T if temps else None)
-    rh, rw = o_backward(H.cpu(), W.cpu(), ids.cpu(), gl.cpu(), ge.cpu() if ent else None, 1.0,
-                        T.cpu() if temps else None)
-    assert _rel(dh.cpu().double().numpy(), rh) <= TOL
-    assert _rel(dw.cpu().double().numpy(), rw) <= TOL
-    # row-wise too: no token's gradient is off
-    eh = np.linalg.norm(dh.cpu().double().numpy() - rh, axis=1) / np.maximum(np.linalg.norm(rh, axis=1), 1e-30)
-    assert eh.max() <= 4 * TOL
+    ge_, T_ = (ge if ent else None), (T if temps else None)
+    dh, dw = tim.head_backward(H, W, ids, gl, ge_, 1.0, T_)
+    rh, rw = o_backward(H.cpu(), W.cpu(), ids.cpu(), gl.cpu(), None if ge_ is None else ge_.cpu(), 1.0,
+                        None if T_ is None else T_.cpu())
+    _, bh, bw = _bounds(H, W, ids, gl, ge_, T_)
+    wh = _assert_within(_np(dh), rh, bh, "dhidden")
+    ww = _assert_within(_np(dw), rw, bw, "dweight")
+    print(f"worst err / bound: dH {wh:.3f} dW {ww:.3f}")
+    assert _rel(_np(dh), rh) <= 4e-3 and _rel(_np(dw), rw) <= 4e-3
 
 
 @pytest.mark.slow
 @pytest.mark.parametrize("d", [2048, 4096])
 def test_backward_full_vocab(tim, d):
-    """BASELINE configs' head (V = 151936) at 512 tokens; dweight compared on sampled rows
-    (the sampled ids plus random rows), dhidden in full."""
-    N, V = 512, 151936
+    """BASELINE configs' head (V = 151936) at 256 tokens, element-wise: dhidden in full, dweight on
+    sampled rows (the sampled ids, random rows, the first and last rows)."""
+    N, V = 256, 151936
     H, W, ids, gl, ge, T = _problem(N, d, V, 40 + d, "peaked")
     dh, dw = tim.head_backward(H, W, ids, gl, ge)
-    G = grad_logits(H.cpu(), W.cpu(), ids.cpu(), gl.cpu(), ge.cpu())
-    rh = G @ W.cpu().double().numpy()
-    assert _rel(dh.cpu().double().numpy(), rh) <= TOL
+    G, bh, bw = _bounds(H, W, ids, gl, ge, None)
+    rh = G @ _np(W)
+    _assert_within(_np(dh), rh, bh, "dhidden")
     rows = np.unique(np.concatenate([ids.cpu().numpy()[:64], np.random.default_rng(0).integers(0, V, 64),
                                      [0, V - 1]]))
-    rw = G[:, rows].T @ H.cpu().double().numpy()
-    assert _rel(dw[torch.as_tensor(rows, device=DEV)].cpu().double().numpy(), rw) <= TOL
+    rw = G[:, rows].T @ _np(H)
+    _assert_within(_np(dw[torch.as_tensor(rows, device=DEV)]), rw, bw[rows], "dweight")
 
 
 def test_zero_gradient_and_determinism(tim):

@@ -151,11 +151,15 @@ def test_pair_and_single_cta_variants_agree_within_tolerance(tim):
 
 def test_special_cases(tim):
     d = 128
-    # V = 1: logp = 0 and H = 0 (exact in the oracle; on the GPU t = fma(z, c, -RN(z c)) is the
-    # rounding error of one fp32 product, so the result is 0 to within ~1e-8)
+    # V = 1: logp = 0 and H = 0 EXACTLY (reading U16): the max column has
+    # t = RN(RN(z c) - m) = 0, so its weight is ex2(0) = 1 and both merges are exact
     H, W, ids = _case(300, d, 1, 9)
-    lp, ent = tim.logprob(H, W, torch.zeros(300, dtype=torch.int64, device=DEV))
-    assert lp.abs().max().item() < 1e-6 and ent.abs().max().item() < 1e-6
+    for T in (1.0, 0.7):
+        lp, ent = tim.logprob(H, W, torch.zeros(300, dtype=torch.int64, device=DEV), temperature=T)
+        assert torch.count_nonzero(lp).item() == 0 and torch.count_nonzero(ent).item() == 0
+        ids1, lps, ents = tim.sample(H, W, torch.arange(300, device=DEV), seed=1, temperature=T)
+        assert torch.count_nonzero(ids1).item() == 0
+        assert torch.count_nonzero(lps).item() == 0 and torch.count_nonzero(ents).item() == 0
     # W == 0: uniform, logp = -ln V, H = ln V
     for V in (2, 257, 151936):
         Wz = torch.zeros(V, d, dtype=torch.bfloat16, device=DEV)

@@ -64,12 +64,23 @@ def test_sample_batch_invariance(tim):
     assert (other != ref[0]).float().mean().item() > 0.5   # flat logits: a new seed redraws
 
 
-@pytest.mark.parametrize("N,d,V", [(128, 256, 1000), (64, 2048, 151936)])
-def test_sample_matches_fp64_oracle_up_to_near_ties(tim, N, d, V):
+@pytest.mark.parametrize("N,d,V,tmode", [(128, 256, 1000, 1.0), (64, 2048, 151936, 1.0), (128, 256, 1000, 0.7),
+                                          (96, 2048, 151936, 0.7), (128, 512, 33000, "per-token")])
+def test_sample_matches_fp64_oracle_up_to_near_ties(tim, N, d, V, tmode):
+    """GPU draw vs oracle.sample (pinned at T != 1 in test_oracle_sample.py) at T = 1, 0.7 and
+    per-token T in [0.5, 1.5]: the same id unless the top two scores are within 1e-3 nats."""
     H, W, keys = _case(N, d, V, 33, "flat")
     seed = 0x1234_5678_9ABC
-    ids, lp, _ = tim.sample(H, W, keys, seed=seed)
-    oid, scores = osm.sample(H.cpu(), W.cpu(), keys.cpu().numpy(), seed)
+    if tmode == "per-token":
+        temps = (0.5 + torch.rand(N, generator=torch.Generator().manual_seed(5))).to(DEV)
+        ids, lp, _ = tim.sample(H, W, keys, seed=seed, temperatures=temps)
+        oid, scores = osm.sample(H.cpu(), W.cpu(), keys.cpu().numpy(), seed, temperatures=temps.cpu())
+        lp2, _ = tim.logprob(H, W, ids, temperatures=temps)
+    else:
+        ids, lp, _ = tim.sample(H, W, keys, seed=seed, temperature=tmode)
+        oid, scores = osm.sample(H.cpu(), W.cpu(), keys.cpu().numpy(), seed, temperature=tmode)
+        lp2, _ = tim.logprob(H, W, ids, temperature=tmode)
+    assert torch.equal(_bits(lp), _bits(lp2))
     ids = ids.cpu().numpy()
     rows = np.arange(N)
     top = scores.max(axis=1)
