@@ -46,6 +46,13 @@ tim_status tim_debug_set_schedule(int32_t group, int32_t demote);
  * the live hidden-state tiles of all pairs fit in L2). */
 tim_status tim_debug_set_cluster(int32_t pairs_per_cluster);
 
+/* Head-backward GEMM knob (never changes results): a CTA pair may run at most k_blocks 64-wide
+ * K blocks ahead of the slowest pair (0 = no gate).  Default 128. */
+tim_status tim_debug_set_gemm_slack(int32_t k_blocks);
+/* L2 eviction policy of the backward GEMMs' operand loads (1 evict_normal, 2 evict_first, 3
+ * evict_last) for dH's A (= G) / B (= W) and dW's A (= G^T) / B (= H).  Default 1, 1, 1, 3. */
+tim_status tim_debug_set_gemm_policy(int32_t dh_a, int32_t dh_b, int32_t dw_a, int32_t dw_b);
+
 #ifdef __cplusplus
 }
 #endif

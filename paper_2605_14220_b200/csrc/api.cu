@@ -45,13 +45,21 @@ std::atomic<int> g_sync_slack{4};    // pairs stay within 4 vocab tiles of each 
 std::atomic<int> g_group{0};         // pairs per M-tile group (0 = automatic from the L2 size)
 std::atomic<int> g_demote{0};        // demote finished H tiles to evict_normal (applypriority)
 std::atomic<int> g_quad{0};          // 2-pair clusters sharing W tiles through TMA multicast
+// backward GEMMs: pairs stay within 128 k-blocks of each other; L2 policies dH A / B, dW A / B
+// (H evict_last: the <= 115 MB token block is re-read by every wave).  Interleaved A/B over slack
+// {0, 32, 128} x policies: within 3-5%, this the fastest (profiles/r02_gemm_knobs_ab.txt).
+std::atomic<int> g_gemm_slack{128};
+std::atomic<int> g_gemm_pol[4] = {{1}, {1}, {1}, {3}};
 
 struct Knobs {
-  int use_pair, pad_small, max_clusters, h_policy, w_policy, sleep_waits, sync_slack, group, demote, quad;
+  int use_pair, pad_small, max_clusters, h_policy, w_policy, sleep_waits, sync_slack, group, demote, quad, gemm_slack;
+  int gemm_pol[4];
 };
 Knobs knobs() {
   return Knobs{g_use_pair.load(), g_pad_small.load(), g_max_clusters.load(), g_h_policy.load(), g_w_policy.load(),
-               g_sleep_waits.load(), g_sync_slack.load(), g_group.load(), g_demote.load(), g_quad.load()};
+               g_sleep_waits.load(), g_sync_slack.load(), g_group.load(), g_demote.load(), g_quad.load(),
+               g_gemm_slack.load(), {g_gemm_pol[0].load(), g_gemm_pol[1].load(), g_gemm_pol[2].load(),
+                                     g_gemm_pol[3].load()}};
 }
 
 tim_status device_info(DevInfo** out) {
@@ -894,18 +902,23 @@ static tim_status head_backward_impl(const void* hidden_bf16, int64_t ld_hidden,
     //     order (ascending V in steps of 16) is a constant of (V, d): batch-invariant rows.
     int max_pairs = dev->max_pair_clusters;
     if (kn.max_clusters > 0 && kn.max_clusters < max_pairs) max_pairs = kn.max_clusters;
+    uint32_t* prog = reinterpret_cast<uint32_t*>(fwd_ws + kWsProgressOffset);  // per-pair gate counters
     if (dhidden_or_null) {
       CUtensorMap ta, tb;
       if (!encode_bf16_2d(&ta, G, nbc, vocab, g_ld, 128)) return TIM_ERR_CUDA;        // A = G, K-major
       if (!encode_bf16_2d(&tb, weight_bf16, vocab, d, d, 64)) return TIM_ERR_CUDA;    // B = W, MN-major
-      BwdGemmParams gp{dhidden_or_null + b0 * d, d, static_cast<int>(nbc), d, vocab};
+      if (cudaMemsetAsync(prog, 0, kWsHeaderBytes - kWsProgressOffset, s) != cudaSuccess) return TIM_ERR_CUDA;
+      BwdGemmParams gp{dhidden_or_null + b0 * d, d, static_cast<int>(nbc), d, vocab, prog, kn.gemm_slack,
+                       kn.gemm_pol[0], kn.gemm_pol[1]};
       if (launch_bwd_gemm_dh(ta, tb, gp, max_pairs, s) != cudaSuccess) return TIM_ERR_CUDA;
     }
     if (dweight_or_null) {
       CUtensorMap ta, tb;
       if (!encode_bf16_2d(&ta, G, nbc, vocab, g_ld, 64)) return TIM_ERR_CUDA;         // A = G^T, MN-major
       if (!encode_bf16_2d(&tb, hb, nbc, d, ld_hidden, 64)) return TIM_ERR_CUDA;       // B = H, MN-major
-      BwdGemmParams gp{dweight_or_null, d, vocab, d, static_cast<int>(nbc)};
+      if (cudaMemsetAsync(prog, 0, kWsHeaderBytes - kWsProgressOffset, s) != cudaSuccess) return TIM_ERR_CUDA;
+      BwdGemmParams gp{dweight_or_null, d, vocab, d, static_cast<int>(nbc), prog, kn.gemm_slack, kn.gemm_pol[2],
+                       kn.gemm_pol[3]};
       if (launch_bwd_gemm_dw(ta, tb, gp, max_pairs, s) != cudaSuccess) return TIM_ERR_CUDA;
     }
   }
@@ -1108,6 +1121,20 @@ tim_status tim_debug_set_schedule(int32_t group, int32_t demote) {
   if (group != 0 && group != 1 && group != 2 && group != 4 && group != 8) return TIM_ERR_VALUE;
   g_group = group;
   g_demote = demote != 0;
+  return TIM_OK;
+}
+
+tim_status tim_debug_set_gemm_slack(int32_t k_blocks) {
+  if (k_blocks < 0) return TIM_ERR_VALUE;
+  g_gemm_slack = k_blocks;
+  return TIM_OK;
+}
+
+tim_status tim_debug_set_gemm_policy(int32_t dh_a, int32_t dh_b, int32_t dw_a, int32_t dw_b) {
+  const int32_t v[4] = {dh_a, dh_b, dw_a, dw_b};
+  for (int i = 0; i < 4; ++i)
+    if (v[i] < 1 || v[i] > 3) return TIM_ERR_VALUE;
+  for (int i = 0; i < 4; ++i) g_gemm_pol[i] = v[i];
   return TIM_OK;
 }
 

@@ -59,6 +59,41 @@ __device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t smem_addr, uint3
   return d;
 }
 
+__device__ __forceinline__ void st_relaxed_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t gtimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Whole producer warp: wait (at most ~200 us) until every pair has issued `target` k-blocks;
+// returns the observed minimum.  A throttle only -- results never depend on it.
+__device__ __noinline__ uint32_t gemm_wait_progress(const uint32_t* prog, uint32_t ncl, uint32_t target, int lane) {
+  const uint64_t t0 = gtimer_ns();
+  uint32_t mn;
+  while (true) {
+    mn = 0xFFFFFFFFu;
+    for (uint32_t c = lane; c < ncl; c += 32) {
+      const uint32_t v = ld_relaxed_u32(prog + c);
+      mn = v < mn ? v : mn;
+    }
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    if (mn >= target || gtimer_ns() - t0 > 200000ull) break;
+    __nanosleep(128);
+  }
+  return mn;
+}
+
+__device__ __forceinline__ uint64_t gemm_policy(int kind) {
+  return kind == 3 ? policy_evict_last() : kind == 2 ? policy_evict_first() : policy_evict_normal();
+}
+
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
   asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
                : "memory");
@@ -119,12 +154,27 @@ __global__ void __launch_bounds__(kGThreads, 1)
   if (warp == 0) {
     // ===================== TMA producer (whole warp; one elected lane issues) =====================
     uint32_t stage = 0, phase = 0;
-    const uint64_t pol = policy_evict_normal();
+    // L2 policies of the two operand streams (host-chosen, tim_debug_set_gemm_policy)
+    const uint64_t pol_a = gemm_policy(p.a_policy);
+    const uint64_t pol_b = gemm_policy(p.b_policy);
+    // progress gate (performance only): the pairs sharing an A or B stream read the same k-block
+    // within `sync_slack` k-blocks of each other, so a stream is fetched from DRAM about once per
+    // wave instead of once per pair (ncu, dH at C1's 14080-token block: DRAM 22 -> 8.3 GB)
+    const bool publish = prank == 0 && p.sync_slack > 0 && p.progress != nullptr;
+    bool gate = publish;
+    uint32_t step = 0, known_min = 0;
     for (int tile = static_cast<int>(cid); tile < n_tiles; tile += static_cast<int>(ncl)) {
       const int mt = tile / n_nt, nt = tile % n_nt;
       const int m0 = mt * 2 * kGCtaM + static_cast<int>(prank) * kGCtaM;   // this CTA's A rows
       const int n0 = nt * kGTileN + static_cast<int>(prank) * (kGTileN / 2);  // this CTA's half of B
-      for (int kb = 0; kb < nkb; ++kb) {
+      for (int kb = 0; kb < nkb; ++kb, ++step) {
+        if (gate && (step & 7u) == 0u) {
+          if (lane == 0) st_relaxed_u32(p.progress + cid, step);
+          if (step > known_min + static_cast<uint32_t>(p.sync_slack)) {
+            known_min = gemm_wait_progress(p.progress, ncl, step - p.sync_slack, lane);
+            if (known_min + static_cast<uint32_t>(p.sync_slack) < step) gate = false;  // a pair never showed up
+          }
+        }
         mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
         const uint32_t fb_local = smem_u32(&full[stage]);
         if (leader) mbar_arrive_expect_tx_elect(fb_local, 2 * kGStageBytes);
@@ -133,17 +183,18 @@ __global__ void __launch_bounds__(kGThreads, 1)
         const uint32_t b_dst = smem_u32(smem_b + stage * kGBBytes);
         const int k0 = kb * kGBlockK;
         if (kAMN) {  // G^T: box {64 vocab columns, 64 token rows} x 2
-          tma_load_2d_pair_hint_elect(a_dst, &tmap_a, fb, m0, k0, pol);
-          tma_load_2d_pair_hint_elect(a_dst + kMnChunkBytes, &tmap_a, fb, m0 + 64, k0, pol);
+          tma_load_2d_pair_hint_elect(a_dst, &tmap_a, fb, m0, k0, pol_a);
+          tma_load_2d_pair_hint_elect(a_dst + kMnChunkBytes, &tmap_a, fb, m0 + 64, k0, pol_a);
         } else {     // G: box {64 K columns, 128 token rows}
-          tma_load_2d_pair_hint_elect(a_dst, &tmap_a, fb, k0, m0, pol);
+          tma_load_2d_pair_hint_elect(a_dst, &tmap_a, fb, k0, m0, pol_a);
         }
-        tma_load_2d_pair_hint_elect(b_dst, &tmap_b, fb, n0, k0, pol);
-        tma_load_2d_pair_hint_elect(b_dst + kMnChunkBytes, &tmap_b, fb, n0 + 64, k0, pol);
+        tma_load_2d_pair_hint_elect(b_dst, &tmap_b, fb, n0, k0, pol_b);
+        tma_load_2d_pair_hint_elect(b_dst + kMnChunkBytes, &tmap_b, fb, n0 + 64, k0, pol_b);
         __syncwarp();
         if (++stage == kGStages) { stage = 0; phase ^= 1; }
       }
     }
+    if (publish && lane == 0) st_relaxed_u32(p.progress + cid, 0xFFFFFFFFu);
   } else if (warp == 1) {
     // ===================== MMA issuer (the leader CTA's warp 1) =====================
     if (leader) {

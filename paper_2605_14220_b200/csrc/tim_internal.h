@@ -123,6 +123,9 @@ struct BwdGemmParams {
   float* c;
   int64_t ldc;
   int m, n, k;
+  uint32_t* progress;  // [pairs] k-blocks issued per CTA pair (zeroed per launch), or null: no gate
+  int sync_slack;      // max k-blocks a pair may run ahead of the slowest (0 = no gate)
+  int a_policy, b_policy;  // L2 policy of the A / B tile loads: 1 normal, 2 evict_first, 3 evict_last
 };
 cudaError_t launch_bwd_gemm_dh(const CUtensorMap& tg_kmajor, const CUtensorMap& tw_mn, const BwdGemmParams& p,
                                int max_pairs, cudaStream_t stream);

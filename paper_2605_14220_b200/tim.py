@@ -106,6 +106,8 @@ _SIGS = {
     "tim_debug_set_tuning": (_I32, [_I32, _I32, _I32, _I32]),
     "tim_debug_set_schedule": (_I32, [_I32, _I32]),
     "tim_debug_set_cluster": (_I32, [_I32]),
+    "tim_debug_set_gemm_slack": (_I32, [_I32]),
+    "tim_debug_set_gemm_policy": (_I32, [_I32, _I32, _I32, _I32]),
 }
 
 _lib = None
@@ -474,6 +476,16 @@ def debug_set_schedule(group: int = 0, demote: bool = False):
 def debug_set_cluster(pairs_per_cluster: int = 1):
     """Cluster shape knob (results unchanged): 2 = two CTA pairs sharing W through TMA multicast."""
     _check(lib().tim_debug_set_cluster(int(pairs_per_cluster)), "tim_debug_set_cluster")
+
+
+def debug_set_gemm_slack(k_blocks: int = 128):
+    """Head-backward GEMM progress gate (tim_debug_set_gemm_slack); never changes a result bit."""
+    _check(lib().tim_debug_set_gemm_slack(int(k_blocks)), "tim_debug_set_gemm_slack")
+
+
+def debug_set_gemm_policy(dh_a: int = 1, dh_b: int = 1, dw_a: int = 1, dw_b: int = 3):
+    """Head-backward GEMM L2 policies (tim_debug_set_gemm_policy); never changes a result bit."""
+    _check(lib().tim_debug_set_gemm_policy(int(dh_a), int(dh_b), int(dw_a), int(dw_b)), "tim_debug_set_gemm_policy")
 
 
 def debug_set_pad_small(enable: bool = True):
