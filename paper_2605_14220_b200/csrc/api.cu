@@ -280,6 +280,7 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   p.hidden_ptr = h_tma;
   p.ld_hidden_bytes = h_ld * 2;
   p.demote = kn.demote;
+  p.gate_stats = &hdr->reserved[5];  // read back by the diagnostics scripts (zeroed with the header)
   p.row_keys = row_keys;
   p.seed = seed;
   p.partials2 = sample ? partials + static_cast<size_t>(vocab_slices(vocab)) * static_cast<size_t>(n_tok) : nullptr;

@@ -376,7 +376,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           // a pair that never shows up (not co-resident: another kernel holds SMs, or a cluster
           // shape the GPU cannot place everywhere) must not throttle us: stop gating after a
           // timed-out wait
-          if (known_min + p.sync_slack < step) gate = false;
+          if (known_min + p.sync_slack < step) {
+            gate = false;
+            if (lane == 0 && p.gate_stats) atomicAdd(p.gate_stats, 1ull);  // diagnostics: gates given up
+          }
         }
         const int n0 = vt * kTileN - p.w_row0 + prank * C::kBRows + (kNP == 2 ? pid * (C::kBRows / 2) : 0);
         for (int kb = 0; kb < nkb; ++kb) {

@@ -51,6 +51,7 @@ struct LogprobParams {
   const void* hidden_ptr;    // H base (for L2 priority demotion of finished M-tiles)
   int64_t ld_hidden_bytes;
   int demote;                // demote finished H tiles to evict_normal
+  unsigned long long* gate_stats;  // diagnostics: number of progress gates given up (timed out)
   // head backward (NEXT-3) gradient epilogue
   const float* grad_logp;    // [n_tok] dL/dlogp
   const float* grad_ent;     // [n_tok] dL/dH or null

@@ -1,0 +1,8 @@
+#!/bin/bash
+mkdir -p gpurun_out
+export PYTHONPATH=$PWD
+for t in default 3,2,0,8 3,2,0,16 3,2,0,4,4; do
+timeout -s KILL 300 python scripts/c2_diag.py 2097152 $t 4 >> gpurun_out/c2_diag.txt 2>&1
+done
+timeout -s KILL 600 ncu --metrics gpu__time_duration.sum,sm__cycles_elapsed.avg.per_second,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,dram__bytes_read.sum,lts__t_sector_hit_rate.pct --clock-control none --csv -k regex:logprob_fwd -c 3 \
+   --log-file gpurun_out/c2_ncu_default.csv python scripts/c2_diag.py 2097152 default 3 > gpurun_out/c2_ncu_default.txt 2>&1

@@ -171,3 +171,25 @@ def test_saved_forward_backward(tim, N, d, V):
     b = tim.head_backward(H, W, ids, gl, ge, 1.0, T, saved=(ent, lse2))
     for x, y in zip(a, b):
         assert torch.equal(x.view(torch.int32), y.view(torch.int32))
+
+
+def test_dhidden_is_batch_invariant(tim):
+    """dH[t] = sum_v G[t, v] W[v] is one fixed-order (K = V ascending, K = 16 steps) tensor-core
+    accumulation per element on the hand-written tcgen05 GEMM, and G[t] depends only on row t:
+    the same token's dH is bitwise equal alone, in any pack, in any row slot, and when the batch
+    spans several token blocks (§3.1 P:202-207 invariance, extended to the backward)."""
+    N, d, V = 700, 256, 151936
+    H, W, ids, gl, ge, T = _problem(N, d, V, 31, "peaked")
+    ref, _ = tim.head_backward(H, W, ids, gl, ge, 1.0, T, need_dweight=False)
+    bits = ref.view(torch.int32)
+    for a, b in ((0, 1), (5, 6), (0, 255), (255, 700), (3, 390), (699, 700)):
+        got, _ = tim.head_backward(H[a:b], W, ids[a:b], gl[a:b], ge[a:b], 1.0, T[a:b], need_dweight=False)
+        assert torch.equal(got.view(torch.int32), bits[a:b]), (a, b)
+    perm = torch.randperm(N, generator=torch.Generator().manual_seed(2)).to(DEV)
+    got, _ = tim.head_backward(H[perm], W, ids[perm], gl[perm], ge[perm], 1.0, T[perm], need_dweight=False)
+    assert torch.equal(got.view(torch.int32), bits[perm])
+    from paper_2605_14220_b200.tim import debug_set_kernel
+    debug_set_kernel(True, 5)   # a 5-pair grid: other tiles per pair, same bits
+    got, _ = tim.head_backward(H, W, ids, gl, ge, 1.0, T, need_dweight=False)
+    debug_set_kernel(True, 0)
+    assert torch.equal(got.view(torch.int32), bits)
