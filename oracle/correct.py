@@ -12,8 +12,9 @@ Real-number semantics from PAPER.md:
 Because integer outputs (masks, counts) must be bit-exact between this oracle
 and the GPU, they are defined by the decision-path arithmetic contract of
 SURVEY.md §8(c) C.3, which is written out here step by step.  Every floating
-operation below is ONE IEEE binary64 round-to-nearest numpy ufunc (no fused
-multiply-add: numpy never fuses separate ufunc calls).
+operation below is ONE IEEE binary64 round-to-nearest numpy ufunc (numpy never
+fuses separate ufunc calls), except the K3 series' Horner steps, which are
+single-rounding fused multiply-adds written out by `fma` (exact emulation).
 
   C.3.1  delta = (double)lp_num - (double)lp_den
   C.3.2  non-finite delta -> data error carrying the first bad (global) index
@@ -23,7 +24,9 @@ multiply-add: numpy never fuses separate ufunc calls).
   C.3.5  K1 = -delta
   C.3.6  K3 = k3_c(delta): |delta| <= 1: delta^2 * P(delta), P the Horner
          series of (e^x - 1 - x)/x^2 with coefficients RN(1/n!), n = 2..9 for
-         |delta| <= 2^-6, 2..15 for |delta| <= 2^-2, 2..23 for |delta| <= 1;
+         |delta| <= 2^-6, 2..15 for |delta| <= 2^-2, 2..23 for |delta| <= 1,
+         each Horner step ONE fused multiply-add RN(P * delta + 1/n!) (`fma`,
+         emulated exactly here, DFMA on the GPU; contract revision 4);
          otherwise (exp_c(delta) - 1) - delta.  exp_c = (1 + delta) + K3 for
          |delta| <= 2^-2 (same series), else Cody-Waite reduction
          k = rint(delta * log2 e), r = (delta - k*ln2_hi) - k*ln2_lo, degree-13
@@ -95,11 +98,56 @@ SMALL = 2.0 ** -6  # |delta| <= SMALL: short Horner polynomial n = 2..9 (truncat
 MID = 2.0 ** -2    # |delta| <= MID:   n = 2..15 (first dropped term < 4e-22 relative)
 
 
+def _two_sum(a, b):
+    """Knuth's TwoSum: s = RN(a + b) and the exact error e, a + b = s + e."""
+    s = a + b
+    bb = s - a
+    return s, (a - (s - bb)) + (b - bb)
+
+
+def _split(a):
+    """Veltkamp split: a = hi + lo exactly, each half with at most 26 significant bits."""
+    c = 134217729.0 * a  # 2^27 + 1
+    hi = c - (c - a)
+    return hi, a - hi
+
+
+def _two_prod(a, b):
+    """Dekker's product: p = RN(a b) and the exact error e, a b = p + e (no over- / underflow)."""
+    p = a * b
+    ah, al = _split(a)
+    bh, bl = _split(b)
+    return p, ((ah * bh - p) + ah * bl + al * bh) + al * bl
+
+
+def fma(a, b, c) -> np.ndarray:
+    """RN(a * b + c) with ONE rounding (IEEE 754 fusedMultiplyAdd; the GPU's DFMA), which numpy
+    does not expose.  Boldo & Melquiond's emulation through rounding to odd: uh + ul = a b and
+    th + tl = c + uh exactly, v = RO(tl + ul), result RN(th + v).  Valid for finite operands whose
+    product neither overflows nor underflows (here |a|, |c| <= 1 and |b| >= 2^-150 or b == 0: the
+    contract's Horner steps).  Round to odd of x + y: RN, and when inexact with an even last bit,
+    the neighbour on the side of the exact sum (which has an odd last bit).
+
+    Pinned by: test_oracle_correct.py::test_fma_is_the_correctly_rounded_exact_value (exact rationals,
+    incl. constructed ties and near-ties).
+    """
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    c = np.asarray(c, dtype=np.float64)
+    uh, ul = _two_prod(a, b)
+    th, tl = _two_sum(c, uh)
+    v, e = _two_sum(tl, ul)
+    even = (v.view(np.int64) & 1) == 0
+    v = np.where((e != 0) & even, np.nextafter(v, np.where(e > 0, np.inf, -np.inf)), v)
+    return th + v
+
+
 def _k3_series(d, top: int) -> np.ndarray:
-    """d^2 Q(d), Q = Horner of (e^x - 1 - x)/x^2 with coefficients RN(1/n!), n = top..2."""
+    """d^2 Q(d), Q = Horner of (e^x - 1 - x)/x^2 with coefficients RN(1/n!), n = top..2; every
+    Horner step is one fused multiply-add Q <- RN(Q d + 1/n!) (contract revision 4)."""
     Q = np.full_like(d, INV_FACT[top])
     for n in range(top - 1, 1, -1):
-        Q = Q * d + INV_FACT[n]
+        Q = fma(Q, d, INV_FACT[n])
     return (d * d) * Q
 
 

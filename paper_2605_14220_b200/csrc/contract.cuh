@@ -1,6 +1,7 @@
 // contract.cuh -- device side of the decision-path arithmetic contract (DESIGN.md §2 C.3) and the
 // exact-integer reduction helpers shared by the correction (correct.cu) and PPO (ppo.cu) kernels.
-// Every fp64 op is an explicit round-to-nearest intrinsic (never contracted to FMA); every sum of
+// Every fp64 op is an explicit round-to-nearest intrinsic (__dadd_rn / __dmul_rn are never contracted;
+// the K3 series' Horner steps are explicit single-rounding __fma_rn, contract revision 4); every sum of
 // quantised values is an int128 integer sum, so results do not depend on reduction order,
 // sharding or the number of GPUs.
 #pragma once
@@ -31,12 +32,12 @@ constexpr long long kSatX = 1ll << 62;
 constexpr double kSmall = 0x1p-6;  // |d| <= 2^-6: short Horner polynomial (n = 2..9)
 constexpr double kMid = 0x1p-2;    // |d| <= 2^-2: n = 2..15
 
-// K3 series d^2 Q(d), Q = Horner of RN(1/n!), n = kTop..2.
+// K3 series d^2 Q(d), Q = Horner of RN(1/n!), n = kTop..2, each step one fused multiply-add.
 template <int kTop>
 __device__ __forceinline__ double k3_series(double d) {
   double Q = kInvFact[kTop];
 #pragma unroll
-  for (int n = kTop - 1; n >= 2; --n) Q = __dadd_rn(__dmul_rn(Q, d), kInvFact[n]);
+  for (int n = kTop - 1; n >= 2; --n) Q = __fma_rn(Q, d, kInvFact[n]);
   return __dmul_rn(__dmul_rn(d, d), Q);
 }
 __device__ __forceinline__ double k3_small(double d) { return k3_series<9>(d); }
@@ -44,16 +45,16 @@ __device__ __forceinline__ double k3_mid(double d) { return k3_series<15>(d); }
 __device__ __forceinline__ double k3_medium(double d) { return k3_series<23>(d); }
 
 // The short and mid series of one token in a single Horner chain: the mid prefix (n = 15..10)
-// runs for every token, then a tiny token (|d| <= 2^-6) restarts from RN(0 * d + c9) = c9, which
+// runs for every token, then a tiny token (|d| <= 2^-6) restarts from fma(0, d, c9) = c9, which
 // is exactly the short series' start; n = 8..2 are the same ops for both.  Bit-identical to
 // k3_small (tiny) / k3_mid (otherwise).
 __device__ __forceinline__ double k3_small_or_mid(double d, bool tiny) {
   double P = kInvFact[15];
 #pragma unroll
-  for (int n = 14; n >= 10; --n) P = __dadd_rn(__dmul_rn(P, d), kInvFact[n]);
-  P = __dadd_rn(__dmul_rn(tiny ? 0.0 : P, d), kInvFact[9]);
+  for (int n = 14; n >= 10; --n) P = __fma_rn(P, d, kInvFact[n]);
+  P = __fma_rn(tiny ? 0.0 : P, d, kInvFact[9]);
 #pragma unroll
-  for (int n = 8; n >= 2; --n) P = __dadd_rn(__dmul_rn(P, d), kInvFact[n]);
+  for (int n = 8; n >= 2; --n) P = __fma_rn(P, d, kInvFact[n]);
   return __dmul_rn(__dmul_rn(d, d), P);
 }
 

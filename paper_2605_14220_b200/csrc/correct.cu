@@ -157,7 +157,7 @@ __device__ __forceinline__ void chunk_body(const LocalParams& p, LaneState& st, 
 #pragma unroll
     for (int n = 8; n >= 2; --n)
 #pragma unroll
-      for (int k = 0; k < kTpl; ++k) q[k] = __dadd_rn(__dmul_rn(q[k], ds[k]), kInvFact[n]);
+      for (int k = 0; k < kTpl; ++k) q[k] = __fma_rn(q[k], ds[k], kInvFact[n]);
 #pragma unroll
     for (int k = 0; k < kTpl; ++k) k3s[k] = __dmul_rn(__dmul_rn(ds[k], ds[k]), q[k]);
   }
@@ -294,11 +294,159 @@ __device__ __forceinline__ void chunk_body(const LocalParams& p, LaneState& st, 
   if (kOut) store_chunk(p, i0, full, w_out, c_out, kbits);
 }
 
+// The few tokens of a fast-body chunk that the lock-step body took as delta = 0 (|delta| > 2^-6,
+// or non-finite), redone in their own lanes: the full contract, int128 sums in the lane's
+// shared-memory state, and corrections of what the lock-step body counted for them (a response
+// token, kept, one more contributing token of the sequence).  The chunk lies inside the warp's
+// current sequence, so there is no sequence walk; the scalar stores follow the chunk's vector
+// store in program order.
+template <bool kOut, int kSeqK, bool kTis, bool kTokRs>
+__device__ __forceinline__ void fix_slow(const LocalParams& p, LaneState& st, const unsigned slow, const long long i0,
+                                         const bool sum_on, const double (&dv)[kTpl]) {
+  constexpr bool kSeq = kSeqK != TIM_SEQ_NONE;
+  constexpr bool seq_k1 = kSeqK == TIM_SEQ_K1;
+  const CorrectDevCfg& cfg = p.cfg;
+#pragma unroll
+  for (int k = 0; k < kTpl; ++k) {
+    if (!((slow >> k) & 1u)) continue;
+    const long long i = i0 + k;
+    const double d = dv[k];
+    float w = 1.f, c = 0.f;
+    uint8_t keep8 = 0;
+    if (!isfinite(d)) {  // C.3.2 data error: out of every sum and count, outputs NaN / 0
+      const unsigned long long b = kBadSentinel - static_cast<unsigned long long>(p.tok_begin + i);
+      st.bad_inv = b > st.bad_inv ? b : st.bad_inv;
+      w = CUDART_NAN_F;
+      if (sum_on) {
+        st.c_resp -= 1u;
+        if (kSeq) st.seq_t -= 1;
+      }
+    } else {
+      const double2 ke = k3_exp_full(d);
+      const bool trunc = kTis && d > cfg.log_tis_cap;
+      if (kTis) w = __double2float_rn(trunc ? cfg.tis_cap : fmin(ke.y, cfg.tis_cap));
+      const bool keep = kTokRs ? (cfg.log_lo <= d && d <= cfg.log_hi) : true;
+      c = (sum_on && keep) ? w : 0.f;
+      keep8 = keep ? 1 : 0;
+      if (sum_on) {
+        bool sat1, sat3;
+        const long long x1 = fixed_point(-d, sat1);
+        const long long x3 = fixed_point(ke.x, sat3);
+        st.c_trunc += trunc ? 1u : 0u;
+        st.c_rej += keep ? 0u : 1u;
+        st.s_abs += x1 < 0 ? -x1 : x1;
+        st.s_k1 += x1;
+        st.s_k3 += x3;
+        st.mx = fmax(st.mx, fabs(d));
+        if (kSeq) {
+          if (keep) {
+            const bool satq = seq_k1 ? sat1 : sat3;
+            st.seq_x += seq_k1 ? x1 : x3;
+            st.seq_nsat += satq ? 1 : 0;
+            st.c_sat += satq ? 1 : 0;
+          } else {
+            st.seq_t -= 1;
+          }
+        }
+      }
+    }
+    if (kOut) {
+      p.tis_w[i] = w;
+      p.coeff[i] = c;
+      p.tok_keep[i] = keep8;
+    }
+  }
+}
+
+// The select-free body of a chunk inside one sequence whose response mask is warp-uniform
+// (sum_on: every token a response token, or none), under an interior configuration
+// (LocalParams::interior): every token with |delta| <= 2^-6 runs the short contract series in
+// lock-step (one fused multiply-add per Horner step) and is neither truncated nor token-rejected,
+// and its weight is (float) e^delta.  A token outside that range enters as delta = 0, which adds
+// exactly 0 to every sum, and fix_slow then redoes it.
+template <bool kOut, int kSeqK, bool kTis, bool kTokRs>
+__device__ __forceinline__ void fast_body(const LocalParams& p, LaneState& st, FastAcc& fa, const long long i0,
+                                          const bool sum_on, const double (&dv)[kTpl]) {
+  constexpr bool kSeq = kSeqK != TIM_SEQ_NONE;
+  constexpr bool seq_k1 = kSeqK == TIM_SEQ_K1;
+  double ds[kTpl];
+  unsigned slow = 0;
+#pragma unroll
+  for (int k = 0; k < kTpl; ++k) {
+    const bool sm = fabs(dv[k]) <= kSmall;  // false for NaN
+    slow |= sm ? 0u : (1u << k);
+    ds[k] = sm ? dv[k] : 0.0;
+  }
+  double k3s[kTpl] = {0.0, 0.0, 0.0, 0.0};
+  if (kTis || sum_on) {  // short K3 series, four independent Horner chains
+    double q[kTpl];
+#pragma unroll
+    for (int k = 0; k < kTpl; ++k) q[k] = kInvFact[9];
+#pragma unroll
+    for (int n = 8; n >= 2; --n)
+#pragma unroll
+      for (int k = 0; k < kTpl; ++k) q[k] = __fma_rn(q[k], ds[k], kInvFact[n]);
+#pragma unroll
+    for (int k = 0; k < kTpl; ++k) k3s[k] = __dmul_rn(__dmul_rn(ds[k], ds[k]), q[k]);
+  }
+  float w_out[kTpl], c_out[kTpl];
+#pragma unroll
+  for (int k = 0; k < kTpl; ++k) {
+    w_out[k] = kTis ? __double2float_rn(exp_from_k3_small(ds[k], k3s[k])) : 1.f;
+    c_out[k] = sum_on ? w_out[k] : 0.f;
+  }
+  if (sum_on) {
+#pragma unroll
+    for (int k = 0; k < kTpl; ++k) {
+      const double x1 = rint(__dmul_rn(-ds[k], kTwo52));  // exact scaling, then round to integer
+      const double x3 = rint(__dmul_rn(k3s[k], kTwo52));
+      fa.k1 = __dadd_rn(fa.k1, x1);
+      fa.k3 = __dadd_rn(fa.k3, x3);
+      fa.ab = __dadd_rn(fa.ab, fabs(x1));
+      if (kSeq) fa.seq = __dadd_rn(fa.seq, seq_k1 ? x1 : x3);
+    }
+    const double a01 = fmax(fabs(ds[0]), fabs(ds[1]));
+    const double a23 = fmax(fabs(ds[2]), fabs(ds[3]));
+    fa.mx = fmax(fa.mx, fmax(a01, a23));
+    fa.resp += kTpl;
+    if (kSeq) fa.seq_t += kTpl;
+  }
+  if (kOut) store_chunk(p, i0, true, w_out, c_out, 0x01010101u);
+  if (slow) fix_slow<kOut, kSeqK, kTis, kTokRs>(p, st, slow, i0, sum_on, dv);
+}
+
+// Segmented warp flush of per-lane pending sequence sums (sequence ids non-decreasing in lane
+// order): the head lane of each run of equal ids adds the run's total with one set of atomics.
+__device__ __forceinline__ void seq_flush_segmented(tim_seq_partial* seqp, SeqAcc acc, const int lane) {
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const long long osid = __shfl_down_sync(0xffffffffu, acc.sid, off);
+    const __int128 ox = shfl_down_i128(acc.x, off);
+    const long long ot = __shfl_down_sync(0xffffffffu, acc.t, off);
+    const long long on = __shfl_down_sync(0xffffffffu, acc.nsat, off);
+    if (lane + off < 32 && osid == acc.sid) {
+      acc.x += ox;
+      acc.t += ot;
+      acc.nsat += on;
+    }
+  }
+  // lane l now holds the sum of lanes [l, l+2^k) with the same id, so the head of each run
+  // (first lane of that id) holds the whole run because runs are contiguous.
+  const long long prev_sid = __shfl_up_sync(0xffffffffu, acc.sid, 1);
+  const bool head = lane == 0 || prev_sid != acc.sid;
+  if (head && acc.sid != LLONG_MAX) flush_seq(seqp, acc);
+}
+
 // Pass 1 (a5).  Every warp owns a contiguous run of 128-token chunks (four tokens per lane).
-// The warp streams its chunks' num / den through a kStages-deep ring in shared memory (1-D bulk
-// copies issued by lane 0, completion on one mbarrier per stage), so the bytes in flight do not
-// cost registers; the response mask (128 B per chunk) is prefetched one chunk ahead in a register.
-// Clean chunks (see chunk_body) take the select-free body, the others the masked one.
+// The warp streams its chunks' num / den (and the response mask when 16-B aligned) through a
+// kStages-deep ring in shared memory (1-D bulk copies issued by one elected lane, completion on
+// one mbarrier per stage), so the bytes in flight do not cost registers.  The warp keeps a
+// warp-uniform sequence cursor (w_sid, w_next = cu[w_sid + 1]): a chunk that starts at or after
+// w_next first flushes the warp's pending sums of w_sid (one warp reduction, one set of atomics)
+// and advances the cursor.  A chunk inside w_sid with a warp-uniform response mask takes
+// fast_body; any other chunk (a sequence boundary or a prompt / response boundary inside it, a
+// non-interior configuration) takes the masked body with per-lane sequence walks, after which the
+// lanes are brought back onto one cursor.
 template <bool kOut, int kSeqK, bool kTis, bool kTokRs>
 __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_kernel(LocalParams p) {
   constexpr bool kSeq = kSeqK != TIM_SEQ_NONE;  // kSeqK: the sequence score (TIM_SEQ_K1 / TIM_SEQ_K3)
@@ -319,8 +467,6 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
   st.bad_inv = 0;
   st.c_sat = 0;
   st.seq_nsat = 0;
-  st.sid = LLONG_MAX;
-  st.next_b = LLONG_MAX;
   st.seq_t = 0;
   st.mx = 0.0;
   st.c_resp = st.c_trunc = st.c_rej = 0;
@@ -328,12 +474,13 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
   const long long cpw = (n_chunks + nwarps - 1) / nwarps;
   const long long c_begin = warp_g * cpw;
   const long long c_end = c_begin + cpw < n_chunks ? c_begin + cpw : n_chunks;
-  long long seq_lim = LLONG_MAX;  // a lane chunk at local index i0 >= seq_lim reaches next_b
-  if (kSeq && c_begin < c_end && c_begin * kWarpTok + lane * kTpl < p.n) {
-    st.sid = seq_of(p.cu, p.n_seq, p.tok_begin + c_begin * kWarpTok + lane * kTpl);
-    st.next_b = __ldg(p.cu + st.sid + 1);
-    seq_lim = st.next_b - p.tok_begin - (kTpl - 1);
+  long long w_sid = 0, w_next = LLONG_MAX;  // warp-uniform sequence cursor
+  if (kSeq && c_begin < c_end) {
+    w_sid = seq_of(p.cu, p.n_seq, p.tok_begin + c_begin * kWarpTok);
+    w_next = __ldg(p.cu + w_sid + 1);
   }
+  st.sid = w_sid;  // the masked body's per-lane walk starts from the cursor
+  st.next_b = w_next;
 
   if (blockIdx.x == 0 && threadIdx.x == 0) shard_range_check(p.cu, p.n_seq, p.tok_begin, p.n, st.bad_inv);
 
@@ -346,6 +493,21 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
     st.s_k3 += __double2ll_rn(fa.k3);
     if (kSeq) st.seq_x += __double2ll_rn(fa.seq);
     fa.ab = fa.k1 = fa.k3 = fa.seq = 0.0;
+  };
+  auto pending = [&]() {  // this lane's unflushed sums of sequence st.sid
+    SeqAcc a;
+    a.sid = st.sid;
+    a.x = st.seq_x + __double2ll_rn(fa.seq);
+    a.t = st.seq_t + static_cast<long long>(fa.seq_t);
+    a.nsat = st.seq_nsat;
+    return a;
+  };
+  auto clear_pending = [&]() {
+    st.seq_x = 0;
+    st.seq_t = 0;
+    st.seq_nsat = 0;
+    fa.seq = 0.0;
+    fa.seq_t = 0;
   };
 
   const long long n_vec = p.vec ? p.n / kWarpTok : 0;  // whole, vector-accessible chunks
@@ -400,17 +562,43 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
       j = 0;
       phase ^= 1u;
     }
-    const bool lane_whole = !(kSeq && i0 >= seq_lim);
-    bool lane_fast = lane_whole;
-#pragma unroll
-    for (int k = 0; k < kTpl; ++k) lane_fast = lane_fast && fabs(dv[k]) <= kSmall;  // false for NaN
-    const bool f_all = __all_sync(0xffffffffu, lane_fast && resp == 0x01010101u);
-    const bool f_none = !f_all && __all_sync(0xffffffffu, lane_fast && resp == 0u);
-    if (f_all || f_none) {  // warp-uniform
-      chunk_body<false, kOut, kSeqK, kTis, kTokRs>(p, st, fa, numv, denv, resp, i0, true, true, f_all, dv);
+    const long long g0 = p.tok_begin + c * kWarpTok;
+    bool fast = p.interior != 0;  // warp-uniform
+    if (kSeq && fast) {
+      if (g0 >= w_next) {  // the chunk starts past the cursor's sequence: flush it, advance
+        SeqAcc a = pending();
+        a.x = warp_sum_i128(a.x);
+        a.t = warp_sum_i64(a.t);
+        a.nsat = warp_sum_i64(a.nsat);
+        if (lane == 0) flush_seq(p.seqp, a);
+        clear_pending();
+        while (g0 >= w_next && w_sid + 1 < p.n_seq) {  // skips empty sequences; bounded
+          ++w_sid;
+          w_next = __ldg(p.cu + w_sid + 1);
+        }
+        st.sid = w_sid;
+        st.next_b = w_next;
+      }
+      fast = g0 + (kWarpTok - 1) < w_next;  // no boundary inside the chunk
+    }
+    const bool f_all = fast && __all_sync(0xffffffffu, resp == 0x01010101u);
+    const bool f_none = fast && !f_all && __all_sync(0xffffffffu, resp == 0u);
+    if (f_all || f_none) {
+      fast_body<kOut, kSeqK, kTis, kTokRs>(p, st, fa, i0, f_all, dv);
     } else {
+      const bool lane_whole = !(kSeq && p.tok_begin + i0 + (kTpl - 1) >= st.next_b);
       chunk_body<true, kOut, kSeqK, kTis, kTokRs>(p, st, fa, numv, denv, resp, i0, true, lane_whole, true, dv);
-      if (kSeq) seq_lim = st.next_b - p.tok_begin - (kTpl - 1);
+      if (kSeq && p.interior) {  // back onto one cursor: lane 31 holds the furthest sequence
+        const long long ms = __shfl_sync(0xffffffffu, st.sid, 31);
+        if (__any_sync(0xffffffffu, st.sid != ms)) {
+          seq_flush_segmented(p.seqp, pending(), lane);
+          clear_pending();
+        }
+        w_sid = ms;
+        w_next = __shfl_sync(0xffffffffu, st.next_b, 31);
+        st.sid = w_sid;
+        st.next_b = w_next;
+      }
     }
     if (++cnt == kFoldChunks) {
       fold();
@@ -427,9 +615,8 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
     dv[1] = __dsub_rn(static_cast<double>(cc.num.y), static_cast<double>(cc.den.y));
     dv[2] = __dsub_rn(static_cast<double>(cc.num.z), static_cast<double>(cc.den.z));
     dv[3] = __dsub_rn(static_cast<double>(cc.num.w), static_cast<double>(cc.den.w));
-    const bool lane_whole = full && !(kSeq && i0 >= seq_lim);
+    const bool lane_whole = full && !(kSeq && p.tok_begin + i0 + (kTpl - 1) >= st.next_b);
     chunk_body<true, kOut, kSeqK, kTis, kTokRs>(p, st, fa, cc.num, cc.den, cc.resp, i0, full, lane_whole, true, dv);
-    if (kSeq) seq_lim = st.next_b - p.tok_begin - (kTpl - 1);
     fold();
   }
   fold();
@@ -451,24 +638,7 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
     acc.x = st.seq_x;
     acc.t = st.seq_t;
     acc.nsat = st.seq_nsat;
-    // segmented warp reduction of the open segments (sequence ids are non-decreasing in lane order)
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const long long osid = __shfl_down_sync(0xffffffffu, acc.sid, off);
-      const __int128 ox = shfl_down_i128(acc.x, off);
-      const long long ot = __shfl_down_sync(0xffffffffu, acc.t, off);
-      const long long on = __shfl_down_sync(0xffffffffu, acc.nsat, off);
-      if (lane + off < 32 && osid == acc.sid) {
-        acc.x += ox;
-        acc.t += ot;
-        acc.nsat += on;
-      }
-    }
-    // lane l now holds the sum of lanes [l, l+2^k) with the same id, so the head of each run
-    // (first lane of that id) holds the whole run because runs are contiguous.
-    const long long prev_sid = __shfl_up_sync(0xffffffffu, acc.sid, 1);
-    const bool head = lane == 0 || prev_sid != acc.sid;
-    if (head && acc.sid != LLONG_MAX) flush_seq(p.seqp, acc);
+    seq_flush_segmented(p.seqp, acc, lane);
   }
 
   // block reduction of the global statistics, then one set of integer atomics per block
@@ -638,7 +808,13 @@ __global__ void __launch_bounds__(256) correct_zero_kernel(ZeroParams p) {
   }
 }
 
-cudaError_t launch_correct_local(const LocalParams& p, int num_sms, cudaStream_t stream) {
+cudaError_t launch_correct_local(const LocalParams& p_in, int num_sms, cudaStream_t stream) {
+  LocalParams p = p_in;
+  {  // interior: |delta| <= 2^-6 is never truncated (e^(2^-6) < 1.0158 <= tau) nor token-rejected
+    const CorrectDevCfg& c = p.cfg;
+    p.interior = (!c.tis || (c.log_tis_cap > kSmall && c.tis_cap >= 1.0158)) &&
+                 (!c.tok_rs || (c.log_lo <= -kSmall && c.log_hi >= kSmall));
+  }
   const long long chunks = (p.n + kWarpTok - 1) / kWarpTok;
   const long long warps_per_block = kLocalThreads / 32;
   long long blocks = (chunks + warps_per_block - 1) / warps_per_block;

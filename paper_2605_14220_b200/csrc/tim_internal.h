@@ -154,6 +154,8 @@ struct LocalParams {
   CorrectDevCfg cfg;
   tim_device_status* dstatus;
   int vec;            // every per-token array allows 16-B (4-B for u8) vector accesses
+  int interior;       // set by the launcher: no token with |delta| <= 2^-6 can be truncated or
+                      // token-rejected and min(e^delta, tau) = e^delta there (select-free fast body)
 };
 struct FinishParams {
   const uint8_t* gathered;  // [nranks][block_bytes]

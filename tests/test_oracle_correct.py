@@ -299,3 +299,40 @@ def test_tokens_outside_the_sequences_are_a_data_error():
     assert e.value.index == 101
     # exactly covering shard: fine
     oc.local_partials(np.zeros(4, np.float32), np.zeros(4, np.float32), [0, 50, 104], cfg, None, 100)
+
+
+# ------------------------------------------------ fused multiply-add (C.3 rev. 4) ----
+
+def _fma_exact(a, b, c):
+    """RN(a b + c) of the exact rational (CPython's int / int true division rounds correctly)."""
+    return float(Fraction(float(a)) * Fraction(float(b)) + Fraction(float(c)))
+
+
+def test_fma_is_the_correctly_rounded_exact_value():
+    rng = np.random.default_rng(11)
+    a, b, c = [], [], []
+    # the contract's regime: Horner state Q in (0, 1], d in [-1, 1] at every scale, c = RN(1/n!)
+    for n in range(2, 23):
+        q = rng.uniform(0.0, 1.0, 300)
+        d = rng.uniform(-1, 1, 300) * np.exp2(-rng.integers(0, 150, 300).astype(np.float64))
+        a += list(q); b += list(d); c += [oc.INV_FACT[n]] * 300
+    # general finite operands with every exponent gap between a b and c
+    x = rng.normal(size=3000) * np.exp2(rng.integers(-60, 60, 3000).astype(np.float64))
+    y = rng.normal(size=3000) * np.exp2(rng.integers(-60, 60, 3000).astype(np.float64))
+    z = rng.normal(size=3000) * np.exp2(rng.integers(-180, 120, 3000).astype(np.float64))
+    a += list(x); b += list(y); c += list(z)
+    # exact ties and near-ties that only a single rounding resolves: A, B odd 53-bit integers,
+    # C cancels the top bits of A B so that RN(A B + C) rounds a 54 / 55-bit remainder
+    for k in (54, 55, 56):
+        for _ in range(400):
+            A = int(rng.integers(2 ** 52, 2 ** 53)) | 1
+            B = int(rng.integers(2 ** 52, 2 ** 53)) | 1
+            P = A * B
+            C = -((P >> k) << k)
+            a.append(math.ldexp(A, -53)); b.append(math.ldexp(B, -60)); c.append(math.ldexp(C, -113))
+    a, b, c = np.array(a), np.array(b), np.array(c)
+    got = oc.fma(a, b, c)
+    want = np.array([_fma_exact(*t) for t in zip(a, b, c)])
+    assert np.array_equal(got.view(np.int64), want.view(np.int64))
+    # a plain a * b + c (two roundings) differs on some of these: the test can tell them apart
+    assert not np.array_equal((a * b + c).view(np.int64), want.view(np.int64))
