@@ -531,11 +531,18 @@ def correction_roofline(tim, dev, n, peaks, peak_src, reps=10):
         b.record()
     torch.cuda.synchronize()
     ms = sorted(a.elapsed_time(b) for a, b in evs)[reps // 2]
-    gbs = 18.0 * n / (ms / 1e3) / 1e9
+    # algorithmic bytes: 18 per token for pass 1 (a5) + 4 per token of a rejected sequence for the
+    # coefficient zeroing (a7: "4 B/token only for tokens of rejected sequences")
+    keep = out["seq_keep"].to(torch.int64)
+    lens = (cu[1:] - cu[:-1]).to(torch.int64)
+    n_rej_tok = int(((1 - keep) * lens).sum().item())
+    bpt = 18.0 + 4.0 * n_rej_tok / n
+    gbs = bpt * n / (ms / 1e3) / 1e9
     peak = float(peaks["hbm_gbs"])
     return {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
             "traffic": _hbm_traffic("correct_local_dram_bytes_2e27", n),
-            "n_tok": n, "ms": ms, "algorithmic_bytes_per_token": 18, "peak_source": peak_src + " hbm_gbs",
+            "n_tok": n, "ms": ms, "algorithmic_bytes_per_token": bpt, "tokens_in_rejected_sequences": n_rej_tok,
+            "peak_source": peak_src + " hbm_gbs",
             "kernel": "tim_correct (correct_local + finish + zero, median of %d)" % reps}
 
 

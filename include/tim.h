@@ -298,6 +298,23 @@ tim_status tim_logprob_tp_merge(const void* gathered_partials, int64_t n_tok, in
                                 void* workspace, size_t workspace_bytes,
                                 tim_device_status* dstatus, void* stream);
 
+/* The whole vocab-parallel head in one call: the rank's tim_logprob_tp_partial, the NCCL
+ * all-gather of the slice partials inside the library over `comm` (tp = comm's rank count, this
+ * rank = comm's rank; every rank passes the same n_tok rows and ids), and tim_logprob_tp_merge.
+ * Every rank gets logp / entropy for all n_tok rows, bitwise equal to tim_logprob on the full W.
+ * The exchange carries 16 B per token per slice (S_v n_tok 16 B gathered per rank), stream-ordered
+ * on `stream` like every other call.  Workspace: tim_logprob_tp_workspace_bytes (device, >= 256-B
+ * aligned).  Errors: those of tim_logprob_tp_partial / _merge; TIM_ERR_NCCL if the all-gather
+ * fails; tp must divide S_v. */
+size_t tim_logprob_tp_workspace_bytes(int64_t n_tok, int32_t vocab, int32_t tp);
+tim_status tim_logprob_tp(const void* hidden_bf16, int64_t ld_hidden, const void* weight_shard_bf16,
+                          int32_t hidden, int32_t vocab, tim_comm* comm,
+                          const int64_t* token_ids, int64_t n_tok,
+                          float temperature, const float* temperatures_or_null,
+                          float* logp_out, float* entropy_out_or_null,
+                          void* workspace, size_t workspace_bytes,
+                          tim_device_status* dstatus, void* stream);
+
 /* ----------------------------------------------------------------------------
  * tim_rmsnorm / tim_logprob_rmsnorm  (the batch-invariant RMSNorm
  * prologue of the head, §3.1)

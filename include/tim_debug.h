@@ -53,6 +53,12 @@ tim_status tim_debug_set_gemm_slack(int32_t k_blocks);
  * evict_last) for dH's A (= G) / B (= W) and dW's A (= G^T) / B (= H).  Default 1, 1, 1, 3. */
 tim_status tim_debug_set_gemm_policy(int32_t dh_a, int32_t dh_b, int32_t dw_a, int32_t dw_b);
 
+/* Correction form at P = 1 (never changes results): 1 (default) = the split launches (local,
+ * finish, zero) that P > 1 uses; 0 = pass 1, the sequence decisions and the coefficient zeroing in
+ * ONE cooperative launch behind two grid barriers (SURVEY a7 "fused into pass 1 when P = 1";
+ * measured 2.5% slower at 2^27 tokens, profiles/r02_correction_fused_ab.txt). */
+tim_status tim_debug_set_correct_split(int32_t split);
+
 #ifdef __cplusplus
 }
 #endif

@@ -50,16 +50,19 @@ std::atomic<int> g_quad{0};          // 2-pair clusters sharing W tiles through 
 // {0, 32, 128} x policies: within 3-5%, this the fastest (profiles/r02_gemm_knobs_ab.txt).
 std::atomic<int> g_gemm_slack{128};
 std::atomic<int> g_gemm_pol[4] = {{1}, {1}, {1}, {3}};
+std::atomic<int> g_split_correct{1};  // P = 1 tim_correct: 1 = local + finish + zero launches (default: 2.5%
+                                      // faster than the fused cooperative launch, profiles/r02_correction_fused_ab.txt)
 
 struct Knobs {
   int use_pair, pad_small, max_clusters, h_policy, w_policy, sleep_waits, sync_slack, group, demote, quad, gemm_slack;
   int gemm_pol[4];
+  int split_correct;
 };
 Knobs knobs() {
   return Knobs{g_use_pair.load(), g_pad_small.load(), g_max_clusters.load(), g_h_policy.load(), g_w_policy.load(),
                g_sleep_waits.load(), g_sync_slack.load(), g_group.load(), g_demote.load(), g_quad.load(),
                g_gemm_slack.load(), {g_gemm_pol[0].load(), g_gemm_pol[1].load(), g_gemm_pol[2].load(),
-                                     g_gemm_pol[3].load()}};
+                                     g_gemm_pol[3].load()}, g_split_correct.load()};
 }
 
 tim_status device_info(DevInfo** out) {
@@ -490,10 +493,12 @@ size_t tim_correct_workspace_bytes(int64_t n_tok_local, int64_t n_seq, int32_t n
   return b * (1 + static_cast<size_t>(nranks));  // local block + the all-gathered blocks
 }
 
-tim_status tim_correct_local(const float* num, const float* den, const int64_t* cu, int64_t n_seq,
-                             int64_t tok_begin, int64_t n_local, const uint8_t* resp, const tim_correct_cfg* cfg,
-                             float* tis_w, uint8_t* tok_keep, float* coeff, void* partial_out,
-                             tim_device_status* dstatus, void* stream) {
+// Validate pass-1 arguments, zero the partial block and fill the kernel parameters.
+static tim_status prep_correct_local(const float* num, const float* den, const int64_t* cu, int64_t n_seq,
+                                     int64_t tok_begin, int64_t n_local, const uint8_t* resp,
+                                     const tim_correct_cfg* cfg, float* tis_w, uint8_t* tok_keep, float* coeff,
+                                     void* partial_out, tim_device_status* dstatus, void* stream, LocalParams* out,
+                                     DevInfo** dev_out) {
   tim_status st = check_common(num, den, cu, n_seq, tok_begin, n_local, resp);
   if (st != TIM_OK) return st;
   if ((st = check_cfg(cfg)) != TIM_OK) return st;
@@ -502,12 +507,11 @@ tim_status tim_correct_local(const float* num, const float* den, const int64_t* 
   if (any_out && !(tis_w && tok_keep && coeff)) return TIM_ERR_NULL;
   if (any_out && (!aligned(tis_w, 16) || !aligned(coeff, 16) || !aligned(tok_keep, 8))) return TIM_ERR_ALIGN;
   if (!aligned(partial_out, 16)) return TIM_ERR_ALIGN;
-  DevInfo* dev = nullptr;
-  if ((st = device_info(&dev)) != TIM_OK) return st;
+  if ((st = device_info(dev_out)) != TIM_OK) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (cudaMemsetAsync(partial_out, 0, tim_correct_partial_bytes(n_seq), s) != cudaSuccess) return TIM_ERR_CUDA;
-  if (n_local == 0) return TIM_OK;
-  LocalParams p{};
+  LocalParams& p = *out;
+  p = LocalParams{};
   p.num = num;
   p.den = den;
   p.cu = cu;
@@ -524,7 +528,20 @@ tim_status tim_correct_local(const float* num, const float* den, const int64_t* 
   p.dstatus = dstatus;
   p.vec = aligned(num, 16) && aligned(den, 16) && aligned(resp, 4) && aligned(tis_w, 16) && aligned(coeff, 16) &&
           aligned(tok_keep, 4);
-  return launch_correct_local(p, dev->num_sms, s) == cudaSuccess ? TIM_OK : TIM_ERR_CUDA;
+  return TIM_OK;
+}
+
+tim_status tim_correct_local(const float* num, const float* den, const int64_t* cu, int64_t n_seq,
+                             int64_t tok_begin, int64_t n_local, const uint8_t* resp, const tim_correct_cfg* cfg,
+                             float* tis_w, uint8_t* tok_keep, float* coeff, void* partial_out,
+                             tim_device_status* dstatus, void* stream) {
+  LocalParams p{};
+  DevInfo* dev = nullptr;
+  const tim_status st = prep_correct_local(num, den, cu, n_seq, tok_begin, n_local, resp, cfg, tis_w, tok_keep, coeff,
+                                           partial_out, dstatus, stream, &p, &dev);
+  if (st != TIM_OK || n_local == 0) return st;
+  return launch_correct_local(p, dev->num_sms, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? TIM_OK
+                                                                                                       : TIM_ERR_CUDA;
 }
 
 // scratch: 2 zeroed words for a multi-block finish (or null: one block)
@@ -588,6 +605,40 @@ static tim_status correct_impl(const float* num, const float* den, const int64_t
   if (seq_keep == nullptr && cfg->seq_rs != TIM_SEQ_NONE && tis_w) return TIM_ERR_NULL;
   uint8_t* local = static_cast<uint8_t*>(ws);
   const size_t blk = (tim_correct_partial_bytes(n_seq) + 255) & ~size_t(255);
+  // the local block's header reserved[2..3] (zeroed with the block; pass 1 uses [0..1]) serve as
+  // the finish pass's {ticket, rejections}
+  unsigned long long* scratch =
+      reinterpret_cast<unsigned long long*>(&reinterpret_cast<tim_partial_header*>(local)->reserved[2]);
+  if (comm == nullptr && n_local > 0 && !knobs().split_correct) {
+    // P = 1: pass 1, decisions / stats and the zeroing of rejected sequences in ONE cooperative
+    // launch (a7 "fused into pass 1 when P = 1")
+    LocalParams p{};
+    DevInfo* dev = nullptr;
+    if ((st = prep_correct_local(num, den, cu, n_seq, tok_begin, n_local, resp, cfg, tis_w, tok_keep, coeff, local,
+                                 dstatus, stream, &p, &dev)) != TIM_OK)
+      return st;
+    if (cfg->seq_rs != TIM_SEQ_NONE && tis_w && !seq_keep) return TIM_ERR_NULL;
+    FinishParams f{};
+    f.gathered = local;
+    f.block_bytes = static_cast<int64_t>(tim_correct_partial_bytes(n_seq));
+    f.nranks = 1;
+    f.n_seq = n_seq;
+    f.cfg = dev_cfg(cfg);
+    f.seq_keep = seq_keep;
+    f.seq_score = seq_score;
+    f.stats = stats;
+    f.scratch = scratch;
+    ZeroParams z{};
+    z.cu = cu;
+    z.n_seq = n_seq;
+    z.tok_begin = tok_begin;
+    z.n = n_local;
+    z.seq_keep = seq_keep;
+    z.coeff = coeff;
+    return launch_correct_fused(p, f, z, dev->num_sms, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess
+               ? TIM_OK
+               : TIM_ERR_CUDA;
+  }
   if ((st = tim_correct_local(num, den, cu, n_seq, tok_begin, n_local, resp, cfg, tis_w, tok_keep, coeff, local,
                               dstatus, stream)) != TIM_OK)
     return st;
@@ -602,10 +653,6 @@ static tim_status correct_impl(const float* num, const float* den, const int64_t
       return TIM_ERR_NCCL;
     gathered = g;
   }
-  // the local block's header reserved[2..3] (zeroed with the block; pass 1 uses [0..1]) serve as
-  // the finish pass's {ticket, rejections}
-  unsigned long long* scratch =
-      reinterpret_cast<unsigned long long*>(&reinterpret_cast<tim_partial_header*>(local)->reserved[2]);
   return correct_finish_impl(gathered, nranks, cu, n_seq, tok_begin, n_local, cfg, coeff, seq_keep, seq_score, stats,
                              scratch, stream);
 }
@@ -720,6 +767,40 @@ tim_status tim_logprob_tp_merge(const void* gathered_partials, int64_t n_tok, in
   mp.ws = hdr;
   mp.dstatus = dstatus;
   return launch_logprob_merge(mp, s) == cudaSuccess ? TIM_OK : TIM_ERR_CUDA;
+}
+
+size_t tim_logprob_tp_workspace_bytes(int64_t n_tok, int32_t vocab, int32_t tp) {
+  const size_t part = tim_logprob_tp_partial_bytes(n_tok, vocab, tp);
+  if (n_tok < 0 || vocab < 1 || tp < 1 || vocab_slices(vocab) % tp != 0) return 0;
+  return kWsHeaderBytes + part + part * static_cast<size_t>(tp);  // header, local block, gathered blocks
+}
+
+tim_status tim_logprob_tp(const void* hidden_bf16, int64_t ld_hidden, const void* weight_shard_bf16, int32_t hidden,
+                          int32_t vocab, tim_comm* comm, const int64_t* token_ids, int64_t n_tok, float temperature,
+                          const float* temperatures_or_null, float* logp_out, float* entropy_out_or_null,
+                          void* workspace, size_t workspace_bytes, tim_device_status* dstatus, void* stream) {
+  if (!comm) return TIM_ERR_NULL;
+  const int32_t tp = comm->nranks;
+  if (n_tok < 0 || vocab < 1 || vocab_slices(vocab) % tp != 0) return TIM_ERR_SHAPE;
+  if (n_tok == 0) return TIM_OK;
+  if (!workspace || !logp_out) return TIM_ERR_NULL;
+  if (!aligned(workspace, 256)) return TIM_ERR_ALIGN;
+  if (workspace_bytes < tim_logprob_tp_workspace_bytes(n_tok, vocab, tp)) return TIM_ERR_WORKSPACE;
+  const size_t part = tim_logprob_tp_partial_bytes(n_tok, vocab, tp);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  uint8_t* local = ws + kWsHeaderBytes;
+  uint8_t* gathered = local + part;
+  tim_status st = tim_logprob_tp_partial(hidden_bf16, ld_hidden, weight_shard_bf16, hidden, vocab, tp, comm->rank,
+                                         token_ids, n_tok, temperature, temperatures_or_null, local, ws,
+                                         kWsHeaderBytes, stream);
+  if (st != TIM_OK) return st;
+  NcclApi* api = nccl();
+  if (!api->ok) return TIM_ERR_NCCL;
+  // [tp][S_v / tp][n_tok] in rank order = the full slice-major [S_v][n_tok] array
+  if (api->all_gather(local, gathered, part, kNcclInt8, comm->comm, reinterpret_cast<cudaStream_t>(stream)) != 0)
+    return TIM_ERR_NCCL;
+  return tim_logprob_tp_merge(gathered, n_tok, vocab, token_ids, temperatures_or_null, logp_out, entropy_out_or_null,
+                              ws, kWsHeaderBytes, dstatus, stream);
 }
 
 // --------------------------------------------------------------- RMSNorm (NEXT-4) --
@@ -1136,6 +1217,12 @@ tim_status tim_debug_set_gemm_policy(int32_t dh_a, int32_t dh_b, int32_t dw_a, i
   for (int i = 0; i < 4; ++i)
     if (v[i] < 1 || v[i] > 3) return TIM_ERR_VALUE;
   for (int i = 0; i < 4; ++i) g_gemm_pol[i] = v[i];
+  return TIM_OK;
+}
+
+tim_status tim_debug_set_correct_split(int32_t split) {
+  if (split != 0 && split != 1) return TIM_ERR_VALUE;
+  g_split_correct = split;
   return TIM_OK;
 }
 

@@ -448,7 +448,7 @@ __device__ __forceinline__ void seq_flush_segmented(tim_seq_partial* seqp, SeqAc
 // non-interior configuration) takes the masked body with per-lane sequence walks, after which the
 // lanes are brought back onto one cursor.
 template <bool kOut, int kSeqK, bool kTis, bool kTokRs>
-__global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_kernel(LocalParams p) {
+__device__ __forceinline__ void pass1_body(const LocalParams& p) {
   constexpr bool kSeq = kSeqK != TIM_SEQ_NONE;  // kSeqK: the sequence score (TIM_SEQ_K1 / TIM_SEQ_K3)
   __shared__ LaneState sh_state[kLocalThreads];
   __shared__ __align__(128) float ring[kLocalWarps][kStages][2][kWarpTok];
@@ -699,9 +699,16 @@ __global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_ke
   commit_status_last_block(reinterpret_cast<WsHeader*>(&p.hdr->reserved[0]), p.dstatus);
 }
 
+template <bool kOut, int kSeqK, bool kTis, bool kTokRs>
+__global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_local_kernel(LocalParams p) {
+  pass1_body<kOut, kSeqK, kTis, kTokRs>(p);
+}
+
 constexpr int kFinishThreads = 1024;
 
-__global__ void __launch_bounds__(kFinishThreads) correct_finish_kernel(FinishParams p) {
+// a7 + a8 on the gathered partial blocks: one thread per sequence (grid-stride), the last block
+// to finish (ticket in p.scratch) writes the statistics.
+__device__ __forceinline__ void finish_body(const FinishParams& p) {
   const CorrectDevCfg cfg = p.cfg;
   __shared__ int sh_rej[kFinishThreads / 32];
   int rej = 0;
@@ -796,15 +803,89 @@ __global__ void __launch_bounds__(kFinishThreads) correct_finish_kernel(FinishPa
   }
 }
 
-// Zero the coefficient of this rank's tokens that belong to rejected sequences.
-__global__ void __launch_bounds__(256) correct_zero_kernel(ZeroParams p) {
+__global__ void __launch_bounds__(kFinishThreads) correct_finish_kernel(FinishParams p) { finish_body(p); }
+
+// Zero the coefficient of this rank's tokens that belong to rejected sequences (one block per
+// sequence, grid-stride; 16-B stores between the scalar head and tail).
+__device__ __forceinline__ void zero_body(const ZeroParams& p) {
   const long long te = p.tok_begin + p.n;
   for (long long s = blockIdx.x; s < p.n_seq; s += gridDim.x) {
     if (p.seq_keep[s]) continue;
     const long long c0 = p.cu[s], c1 = p.cu[s + 1], tb = p.tok_begin;
-    const long long a = c0 > tb ? c0 : tb;
-    const long long b = c1 < te ? c1 : te;
-    for (long long g = a + threadIdx.x; g < b; g += blockDim.x) p.coeff[g - p.tok_begin] = 0.f;
+    const long long a = (c0 > tb ? c0 : tb) - tb;  // local token range [a, b)
+    const long long b = (c1 < te ? c1 : te) - tb;
+    if (a >= b) continue;
+    float* c = p.coeff;
+    long long va = (a + 3) & ~3ll, vb = b & ~3ll;  // float4-aligned middle when coeff is 16-B aligned
+    if (va > vb || (reinterpret_cast<uintptr_t>(c) & 15u) != 0) va = vb = b;
+    for (long long i = a + threadIdx.x; i < va; i += blockDim.x) c[i] = 0.f;
+    for (long long i = vb + threadIdx.x; i < b; i += blockDim.x) c[i] = 0.f;
+    for (long long i = va + 4 * threadIdx.x; i < vb; i += 4 * blockDim.x)
+      __stcs(reinterpret_cast<float4*>(c + i), make_float4(0.f, 0.f, 0.f, 0.f));
+  }
+}
+
+__global__ void __launch_bounds__(256) correct_zero_kernel(ZeroParams p) { zero_body(p); }
+
+// Grid-wide barrier of a co-resident (cooperative) grid: one counter, zeroed before the launch,
+// reaches `round` x gridDim.x after the `round`-th barrier.
+__device__ __forceinline__ void grid_barrier(unsigned int* counter, unsigned int round) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(counter, 1u);
+    const unsigned int target = round * gridDim.x;
+    while (atomicAdd(counter, 0u) < target) __nanosleep(64);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// a5 -> a7 -> a8 in ONE launch when P = 1 (SURVEY.md §8(a) a7 "fused into pass 1 when P = 1"):
+// pass 1, a grid barrier, the sequence decisions and statistics on the local partial block, a
+// second barrier, the coefficient zeroing of rejected sequences.  Launched cooperatively (every
+// block resident), so the barriers cannot deadlock; the counter is WsHeader::pad of the local
+// block's header (zeroed with the block).
+template <bool kOut, int kSeqK, bool kTis, bool kTokRs>
+__global__ void __launch_bounds__(kLocalThreads, TIM_CORR_MINB) correct_fused_kernel(LocalParams p, FinishParams f,
+                                                                                      ZeroParams z) {
+  pass1_body<kOut, kSeqK, kTis, kTokRs>(p);
+  unsigned int* bar = &reinterpret_cast<WsHeader*>(&p.hdr->reserved[0])->pad;
+  grid_barrier(bar, 1u);
+  finish_body(f);
+  if (kSeqK != TIM_SEQ_NONE && kOut) {
+    grid_barrier(bar, 2u);
+    // every warp zeroes the rejected tokens of the token range it ran pass 1 on (balanced over
+    // the whole grid), walking the sequences that overlap it
+    const int lane = threadIdx.x & 31;
+    const long long warp_g = (static_cast<long long>(blockIdx.x) * kLocalThreads + threadIdx.x) >> 5;
+    const long long nwarps = (static_cast<long long>(gridDim.x) * kLocalThreads) >> 5;
+    const long long n_chunks = (p.n + kWarpTok - 1) / kWarpTok;
+    const long long cpw = (n_chunks + nwarps - 1) / nwarps;
+    const long long t0 = warp_g * cpw * kWarpTok;
+    long long t1 = t0 + cpw * kWarpTok;
+    if (t1 > p.n) t1 = p.n;
+    if (t0 >= t1) return;
+    const long long tb = p.tok_begin;
+    long long g = tb + t0;
+    long long sq = seq_of(p.cu, p.n_seq, g);
+    float* c = p.coeff;
+    while (g < tb + t1) {
+      const long long sb = __ldg(p.cu + sq), se = __ldg(p.cu + sq + 1);
+      const long long a = (g > sb ? g : sb) - tb;
+      const long long b = (se < tb + t1 ? se : tb + t1) - tb;
+      if (a < b && !z.seq_keep[sq]) {
+        long long va = (a + 3) & ~3ll, vb = b & ~3ll;  // coeff is 16-B aligned (tim_correct checks)
+        if (va > vb) va = vb = b;
+        for (long long i = a + lane; i < va; i += 32) c[i] = 0.f;
+        for (long long i = vb + lane; i < b; i += 32) c[i] = 0.f;
+        for (long long i = va + 4 * lane; i < vb; i += 128)
+          __stcs(reinterpret_cast<float4*>(c + i), make_float4(0.f, 0.f, 0.f, 0.f));
+      }
+      if (sq + 1 >= p.n_seq) break;
+      g = g > se ? g : se;
+      ++sq;
+    }
   }
 }
 
@@ -841,6 +922,53 @@ cudaError_t launch_correct_local(const LocalParams& p_in, int num_sms, cudaStrea
   }
 #undef TIM_CORR_CASE
   return cudaGetLastError();
+}
+
+template <bool kOut, int kSeqK, bool kTis, bool kTokRs>
+static cudaError_t launch_fused_t(const LocalParams& p, const FinishParams& f, const ZeroParams& z, int num_sms,
+                                  cudaStream_t stream) {
+  auto kern = correct_fused_kernel<kOut, kSeqK, kTis, kTokRs>;
+  int per_sm = 0;  // co-resident blocks per SM (the launch fails rather than deadlock if this lies)
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLocalThreads, 0);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorLaunchOutOfResources;
+  const long long chunks = (p.n + kWarpTok - 1) / kWarpTok;
+  long long blocks = (chunks + kLocalWarps - 1) / kLocalWarps;
+  const long long cap = static_cast<long long>(num_sms) * per_sm;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  LocalParams pp = p;
+  FinishParams ff = f;
+  ZeroParams zz = z;
+  void* args[] = {&pp, &ff, &zz};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(static_cast<unsigned>(blocks)),
+                                     dim3(kLocalThreads), args, 0, stream);
+}
+
+cudaError_t launch_correct_fused(const LocalParams& p_in, const FinishParams& f, const ZeroParams& z, int num_sms,
+                                 cudaStream_t stream) {
+  LocalParams p = p_in;
+  {
+    const CorrectDevCfg& c = p.cfg;
+    p.interior = (!c.tis || (c.log_tis_cap > kSmall && c.tis_cap >= 1.0158)) &&
+                 (!c.tok_rs || (c.log_lo <= -kSmall && c.log_hi >= kSmall));
+  }
+  const bool out = p.tis_w != nullptr;
+  const int sk = p.cfg.seq_rs;
+  const int v = (out ? 8 : 0) | (p.cfg.tis ? 2 : 0) | (p.cfg.tok_rs ? 1 : 0);
+#define TIM_FUSED_CASE(o, t, r)                                                                        \
+  case (o ? 8 : 0) | (t ? 2 : 0) | (r ? 1 : 0):                                                        \
+    if (sk == TIM_SEQ_K1) return launch_fused_t<o, TIM_SEQ_K1, t, r>(p, f, z, num_sms, stream);         \
+    if (sk == TIM_SEQ_K3) return launch_fused_t<o, TIM_SEQ_K3, t, r>(p, f, z, num_sms, stream);         \
+    return launch_fused_t<o, TIM_SEQ_NONE, t, r>(p, f, z, num_sms, stream);
+  switch (v) {
+    TIM_FUSED_CASE(true, true, true) TIM_FUSED_CASE(true, true, false)
+    TIM_FUSED_CASE(true, false, true) TIM_FUSED_CASE(true, false, false)
+    TIM_FUSED_CASE(false, true, true) TIM_FUSED_CASE(false, true, false)
+    TIM_FUSED_CASE(false, false, true) TIM_FUSED_CASE(false, false, false)
+  }
+#undef TIM_FUSED_CASE
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_correct_finish(const FinishParams& p, int num_sms, cudaStream_t stream) {

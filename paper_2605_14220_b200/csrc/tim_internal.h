@@ -13,7 +13,7 @@ namespace tim {
 struct WsHeader {
   unsigned long long bad_inv;  // max over bad tokens of (kBadSentinel - index); 0 = no error
   unsigned int counter;        // "last block" ticket
-  unsigned int pad;
+  unsigned int pad;            // the fused correction's grid-barrier counter (correct.cu)
   unsigned long long reserved[6];
 };
 static_assert(sizeof(WsHeader) == 64, "WsHeader size");
@@ -228,5 +228,9 @@ cudaError_t launch_ppo_finish(const PpoFinishParams& p, int num_sms, cudaStream_
 cudaError_t launch_correct_local(const LocalParams& p, int num_sms, cudaStream_t stream);
 cudaError_t launch_correct_finish(const FinishParams& p, int num_sms, cudaStream_t stream);
 cudaError_t launch_correct_zero(const ZeroParams& p, cudaStream_t stream);
+// P = 1: pass 1 + decisions / stats + zeroing in one cooperative launch (grid barriers on the
+// local block header's WsHeader::pad word, zeroed with the block)
+cudaError_t launch_correct_fused(const LocalParams& p, const FinishParams& f, const ZeroParams& z, int num_sms,
+                                 cudaStream_t stream);
 
 }  // namespace tim

@@ -82,6 +82,8 @@ _SIGS = {
     "tim_logprob_tp_partial_bytes": (_SZ, [_I64, _I32, _I32]),
     "tim_logprob_tp_partial": (_I32, [_P, _I64, _P, _I32, _I32, _I32, _I32, _P, _I64, _F, _P, _P, _P, _SZ, _P]),
     "tim_logprob_tp_merge": (_I32, [_P, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _P, _P]),
+    "tim_logprob_tp_workspace_bytes": (_SZ, [_I64, _I32, _I32]),
+    "tim_logprob_tp": (_I32, [_P, _I64, _P, _I32, _I32, _P, _P, _I64, _F, _P, _P, _P, _P, _SZ, _P, _P]),
     "tim_rmsnorm": (_I32, [_P, _I64, _P, _F, _I32, _I64, _P, _P]),
     "tim_logprob_rmsnorm_workspace_bytes": (_SZ, [_I64, _I32, _I32]),
     "tim_logprob_rmsnorm": (_I32, [_P, _I64, _P, _F, _P, _I32, _I32, _P, _I64, _F, _P, _P, _P, _P, _SZ, _P, _P]),
@@ -108,6 +110,7 @@ _SIGS = {
     "tim_debug_set_cluster": (_I32, [_I32]),
     "tim_debug_set_gemm_slack": (_I32, [_I32]),
     "tim_debug_set_gemm_policy": (_I32, [_I32, _I32, _I32, _I32]),
+    "tim_debug_set_correct_split": (_I32, [_I32]),
 }
 
 _lib = None
@@ -345,6 +348,35 @@ def logprob_tp_merge(gathered: torch.Tensor, n_tok: int, vocab: int, ids: torch.
     return lp, ent
 
 
+def logprob_tp(hidden: torch.Tensor, weight_shard: torch.Tensor, vocab: int, ids: torch.Tensor, comm: "Comm",
+               temperature: float = 1.0, temperatures: torch.Tensor | None = None,
+               status: torch.Tensor | None = None):
+    """The whole vocab-parallel head over `comm` (tp = comm.nranks): this rank's slices, the NCCL
+    all-gather of the slice partials inside libtim, the fixed-order merge -- tim_logprob_tp.  Every
+    rank passes the same rows and gets logp / entropy of all of them, bitwise equal to logprob()."""
+    dev = hidden.device
+    N, d = hidden.shape
+    tp, rank = comm.nranks, comm.rank
+    b, e = tp_vocab_range(vocab, tp, rank)
+    if hidden.dtype != torch.bfloat16 or weight_shard.dtype != torch.bfloat16:
+        raise TypeError("hidden and weight_shard must be bfloat16")
+    if weight_shard.dim() != 2 or weight_shard.shape[1] != d or weight_shard.shape[0] != e - b:
+        raise ValueError(f"weight_shard must be W[{b}:{e}] ([{e - b}, {d}]: whole 256-row slices of the fixed "
+                         f"split, tim_tp_vocab_range), got {tuple(weight_shard.shape)}")
+    weight_shard = weight_shard.contiguous()
+    ids = ids.to(device=dev, dtype=torch.int64).contiguous()
+    if temperatures is not None:
+        temperatures = temperatures.to(device=dev, dtype=torch.float32).contiguous()
+    L = lib()
+    lp = torch.empty(N, dtype=torch.float32, device=dev)
+    ent = torch.empty(N, dtype=torch.float32, device=dev)
+    ws = _workspace(dev, max(1024, int(L.tim_logprob_tp_workspace_bytes(N, vocab, tp))), "tp_full")
+    _check(L.tim_logprob_tp(_ptr(hidden), hidden.stride(0), _ptr(weight_shard), d, vocab, comm.handle, _ptr(ids), N,
+                            float(temperature), _ptr(temperatures), _ptr(lp), _ptr(ent), _ptr(ws), ws.numel(),
+                            _ptr(status), _stream(dev)), "tim_logprob_tp")
+    return lp, ent
+
+
 def rmsnorm(hidden: torch.Tensor, gamma: torch.Tensor, eps: float = 1e-6) -> torch.Tensor:
     """Batch-invariant RMSNorm (HF Qwen3 semantics, bf16 in / out) -- tim_rmsnorm."""
     N, d = hidden.shape
@@ -486,6 +518,12 @@ def debug_set_gemm_slack(k_blocks: int = 128):
 def debug_set_gemm_policy(dh_a: int = 1, dh_b: int = 1, dw_a: int = 1, dw_b: int = 3):
     """Head-backward GEMM L2 policies (tim_debug_set_gemm_policy); never changes a result bit."""
     _check(lib().tim_debug_set_gemm_policy(int(dh_a), int(dh_b), int(dw_a), int(dw_b)), "tim_debug_set_gemm_policy")
+
+
+def debug_set_correct_split(split: bool = True):
+    """P = 1 correction form (tim_debug_set_correct_split): True = the split local / finish / zero
+    launches (default, the faster), False = one fused cooperative launch; never changes a result bit."""
+    _check(lib().tim_debug_set_correct_split(int(bool(split))), "tim_debug_set_correct_split")
 
 
 def debug_set_pad_small(enable: bool = True):

@@ -20,6 +20,8 @@ den = -torch.empty(n, device=dev).exponential_(0.7, generator=g)
 num = synth.perturb_laplace_mix(den, 20260004)
 mask = (torch.arange(n, device=dev) % 4096 >= 1024).to(torch.uint8)
 cfg = tim.PRESETS["tis-srs-k3-corr-ratio"]
+if os.environ.get("SPLIT") and hasattr(tim, "debug_set_correct_split"):
+    tim.debug_set_correct_split(os.environ["SPLIT"] == "1")
 out = {"tis_w": torch.empty(n, dtype=torch.float32, device=dev),
        "tok_keep": torch.empty(n, dtype=torch.uint8, device=dev),
        "seq_keep": torch.empty(S, dtype=torch.uint8, device=dev),

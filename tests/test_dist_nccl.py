@@ -6,7 +6,8 @@ into P token shards with cuts inside sequences (tim.shard_range), every rank sco
 tim_logprob, runs tim_correct / tim_ppo_loss with the library's NCCL exchange of exact partials
 (tim.Comm), and rank 0 gathers the per-token outputs.  Everything -- logp, entropy, tis_w,
 tok_keep, coeff, seq_keep, seq_score, the exact statistics, the PPO losses, histograms and
-sequence losses -- must be BITWISE equal to the P = 1 run.
+sequence losses -- must be BITWISE equal to the P = 1 run.  The vocab-parallel head over the same
+communicator (tim_logprob_tp: the library's all-gather of slice partials) must equal tim_logprob.
 
 Collected and run whenever >= 2 GPUs are visible (skipped on a 1-GPU box); the host-side logic
 of the exchange is also covered at world size 2-3 over gloo on the CPU (test_dist_gloo.py).
@@ -71,6 +72,16 @@ def _worker(rank, world, port, outdir):
     pcfg = tim.PPOConfig(eps=0.2, hist_lo=-0.05, hist_hi=0.05, hist_bins=64)
     cur = torch.clamp(lp + 0.01 * noise[a:b].to(dev) * 50, max=0.0)
     ppo = tim.ppo_loss(cur, lp, adv[a:b].to(dev), cu.to(dev), pcfg, coeff=res["coeff"], tok_begin=a, comm=comm)
+    # vocab-parallel head over the same communicator: every rank scores the SAME rows (this rank's
+    # shard of the batch) against its W shard; the library all-gathers the slice partials
+    S_v = tim.vocab_slices(V)
+    if S_v % world == 0:
+        vb, ve = tim.tp_vocab_range(V, world, rank)
+        Hs, ids_s = synth.global_rows(n, D, V, SEED, 0, min(n, 1000), W, device=dev)
+        tlp, tent = tim.logprob_tp(Hs, W[vb:ve].clone(), V, ids_s, comm)
+        rlp, rent = tim.logprob(Hs, W, ids_s)
+        assert torch.equal(tlp.view(torch.int32), rlp.view(torch.int32)), ("tp", world, rank)
+        assert torch.equal(tent.view(torch.int32), rent.view(torch.int32)), ("tp", world, rank)
     torch.cuda.synchronize()
     local = {k: v.cpu() for k, v in (("logp", lp), ("entropy", ent), ("tis_w", res["tis_w"]),
                                        ("tok_keep", res["tok_keep"]), ("coeff", res["coeff"]),

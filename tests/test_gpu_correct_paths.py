@@ -185,3 +185,25 @@ def test_split_form_with_unaligned_cuts(tim, P):
         out = tim.correct_finish(gathered, P, cu.to(DEV), c, locs[r]["coeff"], tok_begin=a)
         assert torch.equal(out["seq_keep"], full["seq_keep"])
         assert torch.equal(locs[r]["coeff"].view(torch.int32), full["coeff"][a:b].view(torch.int32))
+
+
+@pytest.mark.parametrize("kw", CFGS)
+def test_fused_single_launch_equals_split_launches(tim, kw):
+    """P = 1: the cooperative one-launch form (pass 1 + decisions + zeroing behind grid barriers)
+    and the split local / finish / zero launches give the same bits (both also == the oracle)."""
+    from paper_2605_14220_b200.tim import debug_set_correct_split
+    g = np.random.default_rng(12)
+    lens = g.integers(1, 5000, 150)
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    n = int(cu[-1])
+    num, den = _deltas(n, 13, 2e-3)
+    mask = (g.random(n) < 0.9).astype(np.uint8)
+    c = tim.CorrectConfig(**kw)
+    split = _run(tim, num, den, cu, mask, c)
+    try:
+        debug_set_correct_split(False)
+        fused = _run(tim, num, den, cu, mask, c)
+    finally:
+        debug_set_correct_split(True)
+    for k in ("tis_w", "tok_keep", "seq_keep", "coeff", "seq_score", "stats_raw"):
+        assert torch.equal(split[k], fused[k]), k
