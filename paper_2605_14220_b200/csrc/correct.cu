@@ -453,7 +453,6 @@ __device__ __forceinline__ void pass1_body(const LocalParams& p) {
   __shared__ LaneState sh_state[kLocalThreads];
   __shared__ __align__(128) float ring[kLocalWarps][kStages][2][kWarpTok];
   __shared__ __align__(128) uint32_t ring_resp[kLocalWarps][kStages][kWarpTok / 4];
-  __shared__ __align__(8) uint64_t ring_bar[kLocalWarps][kStages];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const long long warp_g = (static_cast<long long>(blockIdx.x) * kLocalThreads + threadIdx.x) >> 5;
@@ -513,55 +512,37 @@ __device__ __forceinline__ void pass1_body(const LocalParams& p) {
   const long long n_vec = p.vec ? p.n / kWarpTok : 0;  // whole, vector-accessible chunks
   long long c_mid = c_end < n_vec ? c_end : n_vec;
   if (c_mid < c_begin) c_mid = c_begin;
-  const uint32_t ring0 = smem_u32(&ring[wib][0][0][0]);
-  const uint32_t bar0 = smem_u32(&ring_bar[wib][0]);
+  // per-lane cp.async ring: lane l copies (and later reads) only its own 4 tokens of each chunk,
+  // so completion is per thread (commit / wait groups) -- no mbarrier, no warp synchronisation
+  const uint32_t ring0 = smem_u32(&ring[wib][0][0][lane * kTpl]);
+  const uint32_t resp0 = smem_u32(&ring_resp[wib][0][lane]);
   const uint64_t pol = policy_evict_first();
-  if (lane == 0) {
-    for (int j = 0; j < kStages; ++j) mbar_init(bar0 + 8 * j, 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
-  // the response mask rides in the ring too when its address allows bulk copies (16-B aligned)
-  const bool resp_bulk = p.resp != nullptr && (reinterpret_cast<uintptr_t>(p.resp) & 15u) == 0;
-  const uint32_t resp0 = smem_u32(&ring_resp[wib][0][0]);
-  auto issue = [&](int j, long long c) {  // whole warp (one elected lane issues): chunk c into stage j
-    const uint32_t dst = ring0 + j * (2 * kWarpTok * 4);
-    mbar_arrive_expect_tx_elect(bar0 + 8 * j, 2 * kWarpTok * 4 + (resp_bulk ? kWarpTok : 0));
-    bulk_g2s_elect(dst, p.num + c * kWarpTok, kWarpTok * 4, bar0 + 8 * j, pol);
-    bulk_g2s_elect(dst + kWarpTok * 4, p.den + c * kWarpTok, kWarpTok * 4, bar0 + 8 * j, pol);
-    if (resp_bulk) bulk_g2s_elect(resp0 + j * kWarpTok, p.resp + c * kWarpTok, kWarpTok, bar0 + 8 * j, pol);
+  const bool has_resp = p.resp != nullptr;
+  auto issue = [&](int j, long long c) {  // chunk c into stage j (one commit group, possibly empty)
+    if (c < c_mid) {
+      const long long i = c * kWarpTok + lane * kTpl;
+      const uint32_t dst = ring0 + j * (2 * kWarpTok * 4);
+      cp_async_16_hint(dst, p.num + i, pol);
+      cp_async_16_hint(dst + kWarpTok * 4, p.den + i, pol);
+      if (has_resp) cp_async_4(resp0 + j * kWarpTok, p.resp + i);
+    }
+    cp_async_commit();
   };
-  for (int j = 0; j < kStages; ++j)
-    if (c_begin + j < c_mid) issue(j, c_begin + j);
-  uint32_t r_nxt = 0x01010101u;
-  if (c_begin < c_mid && p.resp && !resp_bulk)
-    r_nxt = __ldcs(reinterpret_cast<const unsigned int*>(p.resp + c_begin * kWarpTok + lane * kTpl));
+  for (int j = 0; j < kStages; ++j) issue(j, c_begin + j);
   int cnt = 0, j = 0;
-  uint32_t phase = 0;
   for (long long c = c_begin; c < c_mid; ++c) {
     const long long i0 = c * kWarpTok + lane * kTpl;
-    mbar_wait(bar0 + 8 * j, phase);
+    cp_async_wait<kStages - 1>();  // this lane's copies of chunk c have landed
     const float4 numv = *reinterpret_cast<const float4*>(&ring[wib][j][0][lane * kTpl]);
     const float4 denv = *reinterpret_cast<const float4*>(&ring[wib][j][1][lane * kTpl]);
-    uint32_t resp;
-    if (resp_bulk) {
-      resp = ring_resp[wib][j][lane];
-    } else {
-      resp = r_nxt;
-      if (c + 1 < c_mid && p.resp) r_nxt = __ldcs(reinterpret_cast<const unsigned int*>(p.resp + i0 + kWarpTok));
-    }
+    const uint32_t resp = has_resp ? ring_resp[wib][j][lane] : 0x01010101u;
     double dv[kTpl];
     dv[0] = __dsub_rn(static_cast<double>(numv.x), static_cast<double>(denv.x));
     dv[1] = __dsub_rn(static_cast<double>(numv.y), static_cast<double>(denv.y));
     dv[2] = __dsub_rn(static_cast<double>(numv.z), static_cast<double>(denv.z));
     dv[3] = __dsub_rn(static_cast<double>(numv.w), static_cast<double>(denv.w));
-    fence_proxy_async_smem();  // this lane's reads of stage j before the async refill
-    __syncwarp();              // every lane has read stage j: refill it with chunk c + kStages
-    if (c + kStages < c_mid) issue(j, c + kStages);
-    if (++j == kStages) {
-      j = 0;
-      phase ^= 1u;
-    }
+    issue(j, c + kStages);  // the lane has read stage j: refill it (its own slots only)
+    if (++j == kStages) j = 0;
     const long long g0 = p.tok_begin + c * kWarpTok;
     bool fast = p.interior != 0;  // warp-uniform
     if (kSeq && fast) {
