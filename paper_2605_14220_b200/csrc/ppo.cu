@@ -11,9 +11,11 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include <atomic>
 #include <cstdint>
 
 #include "contract.cuh"
+#include "ptx.cuh"
 #include "tim_internal.h"
 
 namespace tim {
@@ -21,11 +23,16 @@ namespace tim {
 constexpr int kPpoTpl = 4;                  // tokens per lane: one float4 of each input
 constexpr int kPpoWarpTok = 32 * kPpoTpl;
 #ifndef TIM_PPO_THREADS
-#define TIM_PPO_THREADS 256
+#define TIM_PPO_THREADS 128
 #endif
 #ifndef TIM_PPO_MINB
-#define TIM_PPO_MINB 2
+#define TIM_PPO_MINB 4
 #endif
+#ifndef TIM_PPO_STAGES
+#define TIM_PPO_STAGES 4
+#endif
+constexpr int kPpoStages = TIM_PPO_STAGES;  // per-warp cp.async ring depth (chunks in flight)
+constexpr int kPpoStageBytes = 4 * 512;     // cur, old, adv, coeff (or the u8 mask): 128 tokens each
 constexpr int kPpoThreads = TIM_PPO_THREADS;
 constexpr int kPpoMinB = TIM_PPO_MINB;
 constexpr int kMaxHistBins = 1024;
@@ -69,6 +76,11 @@ __device__ __forceinline__ PpoChunk ppo_load(const PpoLocalParams& p, long long 
   return c;
 }
 
+// dynamic shared memory: [2][bins + 2] int histogram, then the per-warp rings (16-B aligned)
+__host__ __device__ constexpr size_t ppo_hist_bytes(int bins) {
+  return (sizeof(int) * 2 * static_cast<size_t>(bins + 2) + 15) & ~size_t(15);
+}
+
 __device__ __forceinline__ int hist_slot(const PpoLocalParams& p, double r, double A) {
   const double C = __dmul_rn(-__dsub_rn(r, 1.0), A);
   const double raw = floor(__dmul_rn(__dsub_rn(C, p.hist_lo), p.hist_inv_width));
@@ -81,7 +93,7 @@ __device__ __forceinline__ int hist_slot(const PpoLocalParams& p, double r, doub
 // or loss, non-finite input, partial or unaligned chunk, sequence boundary inside the lane's
 // tokens).
 __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLocalParams p) {
-  extern __shared__ int sh_hist[];  // [2][bins + 2]
+  extern __shared__ __align__(16) int sh_hist[];  // [2][bins + 2], then the rings
   const int nslot = p.bins + 2;
   for (int i = threadIdx.x; i < 2 * nslot; i += blockDim.x) sh_hist[i] = 0;
   __syncthreads();
@@ -111,12 +123,7 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
 
   if (blockIdx.x == 0 && threadIdx.x == 0) shard_range_check(p.cu, p.n_seq, p.tok_begin, p.n, bad_inv);
 
-  PpoChunk nxt;
-  if (c_begin < c_end) nxt = ppo_load(p, c_begin * kPpoWarpTok + lane * kPpoTpl);
-  for (long long ch = c_begin; ch < c_end; ++ch) {
-    const long long i0 = ch * kPpoWarpTok + lane * kPpoTpl;
-    const PpoChunk cur = nxt;
-    if (ch + 1 < c_end) nxt = ppo_load(p, i0 + kPpoWarpTok);
+  auto body = [&](const PpoChunk& cur, const long long i0) {
     const float cu_[4] = {cur.cur.x, cur.cur.y, cur.cur.z, cur.cur.w};
     const float ol_[4] = {cur.old.x, cur.old.y, cur.old.z, cur.old.w};
     const float ad_[4] = {cur.adv.x, cur.adv.y, cur.adv.z, cur.adv.w};
@@ -269,6 +276,56 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
         }
       }
     }
+  };
+
+  // whole vector chunks stream through a per-lane cp.async ring in shared memory (lane l copies and
+  // later reads only its own 4 tokens' slots: completion per thread by commit / wait groups, no
+  // barrier, and the bytes in flight cost no registers); the rest takes element-wise loads
+  const long long n_vec = p.vec ? p.n / kPpoWarpTok : 0;
+  long long c_mid = c_end < n_vec ? c_end : n_vec;
+  if (c_mid < c_begin) c_mid = c_begin;
+  const int wib = threadIdx.x >> 5;
+  uint8_t* ring = reinterpret_cast<uint8_t*>(sh_hist) + ppo_hist_bytes(p.bins) + wib * kPpoStages * kPpoStageBytes;
+  const uint32_t ring16 = smem_u32(ring) + lane * 16;
+  const uint32_t ring4 = smem_u32(ring) + 3 * 512 + lane * 4;
+  const uint64_t pol = policy_evict_first();
+  auto issue = [&](int j, long long c) {  // chunk c into stage j (one commit group, possibly empty)
+    if (c < c_mid) {
+      const long long i = c * kPpoWarpTok + lane * kPpoTpl;
+      const uint32_t d = ring16 + j * kPpoStageBytes;
+      cp_async_16_hint(d, p.cur + i, pol);
+      cp_async_16_hint(d + 512, p.old + i, pol);
+      cp_async_16_hint(d + 1024, p.adv + i, pol);
+      if (p.coeff) cp_async_16_hint(d + 1536, p.coeff + i, pol);
+      else if (p.resp) cp_async_4(ring4 + j * kPpoStageBytes, p.resp + i);
+    }
+    cp_async_commit();
+  };
+  for (int j = 0; j < kPpoStages; ++j) issue(j, c_begin + j);
+  int j = 0;
+  for (long long ch = c_begin; ch < c_mid; ++ch) {
+    cp_async_wait<kPpoStages - 1>();  // this lane's copies of chunk ch have landed
+    const uint8_t* st = ring + j * kPpoStageBytes;
+    PpoChunk c;
+    c.cur = *reinterpret_cast<const float4*>(st + lane * 16);
+    c.old = *reinterpret_cast<const float4*>(st + 512 + lane * 16);
+    c.adv = *reinterpret_cast<const float4*>(st + 1024 + lane * 16);
+    if (p.coeff) {
+      c.w = *reinterpret_cast<const float4*>(st + 1536 + lane * 16);
+    } else if (p.resp) {
+      const uint32_t m = *reinterpret_cast<const uint32_t*>(st + 1536 + lane * 4);
+      c.w = make_float4((m & 0xffu) ? 1.f : 0.f, (m & 0xff00u) ? 1.f : 0.f, (m & 0xff0000u) ? 1.f : 0.f,
+                        (m & 0xff000000u) ? 1.f : 0.f);
+    } else {
+      c.w = make_float4(1.f, 1.f, 1.f, 1.f);
+    }
+    issue(j, ch + kPpoStages);  // the lane has read stage j: refill it
+    if (++j == kPpoStages) j = 0;
+    body(c, ch * kPpoWarpTok + lane * kPpoTpl);
+  }
+  for (long long ch = c_mid; ch < c_end; ++ch) {
+    const long long i0 = ch * kPpoWarpTok + lane * kPpoTpl;
+    body(ppo_load(p, i0), i0);
   }
   // the open sequence segments of the warp (ids are non-decreasing in lane order)
 #pragma unroll
@@ -402,7 +459,19 @@ cudaError_t launch_ppo_local(const PpoLocalParams& p, int num_sms, cudaStream_t 
   const long long cap = static_cast<long long>(num_sms) * kPpoMinB;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  const size_t smem = sizeof(int) * 2 * (p.bins + 2);
+  const size_t smem = ppo_hist_bytes(p.bins) + static_cast<size_t>(kPpoThreads / 32) * kPpoStages * kPpoStageBytes;
+  if (smem > 48 * 1024) {  // the attribute is per device: set it for the current one
+    static std::atomic<bool> attr_set[kMaxDevices];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    if (!attr_set[dev].load()) {
+      e = cudaFuncSetAttribute(ppo_local_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+      attr_set[dev].store(true);
+    }
+  }
   ppo_local_kernel<<<static_cast<int>(blocks), kPpoThreads, smem, stream>>>(p);
   return cudaGetLastError();
 }
