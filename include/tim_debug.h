@@ -59,6 +59,15 @@ tim_status tim_debug_set_gemm_policy(int32_t dh_a, int32_t dh_b, int32_t dw_a, i
  * measured 2.5% slower at 2^27 tokens, profiles/r02_correction_fused_ab.txt). */
 tim_status tim_debug_set_correct_split(int32_t split);
 
+/* Die-aware M-tile groups (never changes results): 1 (default) = when several CTA pairs share an
+ * M-tile (G > 1, d = 4096 batches), pairs on the same die of the B200 form a group, from a one-time
+ * per-device SM -> die latency probe; 0 = groups of consecutive cluster ids. */
+tim_status tim_debug_set_die_groups(int32_t enable);
+/* The probed SM -> die map of the current device (probing it now if needed): state 1 = valid,
+ * -1 = unavailable (then the grouping falls back to cluster-id order); mask_out4[s / 64] bit s % 64
+ * = die of SM s. */
+tim_status tim_debug_die_map(int32_t* state_out, uint64_t* mask_out4);
+
 #ifdef __cplusplus
 }
 #endif

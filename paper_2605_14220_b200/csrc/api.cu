@@ -5,11 +5,13 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <atomic>
 #include <mutex>
+#include <vector>
 
 #include "../../include/tim.h"
 #include "../../include/tim_debug.h"
@@ -27,6 +29,9 @@ struct DevInfo {
   int max_pair_clusters = 0;
   int max_single_ctas = 0;
   int l2_bytes = 0;
+  int dev_id = 0;
+  std::atomic<int> die_state{0};  // SM -> die map: 0 not probed yet, 1 valid, -1 unavailable
+  uint64_t die_mask[4] = {0, 0, 0, 0};
 };
 constexpr int kMaxDev = 64;
 DevInfo g_dev[kMaxDev];
@@ -50,6 +55,7 @@ std::atomic<int> g_quad{0};          // 2-pair clusters sharing W tiles through 
 // {0, 32, 128} x policies: within 3-5%, this the fastest (profiles/r02_gemm_knobs_ab.txt).
 std::atomic<int> g_gemm_slack{128};
 std::atomic<int> g_gemm_pol[4] = {{1}, {1}, {1}, {3}};
+std::atomic<int> g_die_groups{1};     // die-aware M-tile groups (G > 1); 0 = cluster-id order
 std::atomic<int> g_split_correct{1};  // P = 1 tim_correct: 1 = local + finish + zero launches (default: 2.5%
                                       // faster than the fused cooperative launch, profiles/r02_correction_fused_ab.txt)
 
@@ -57,12 +63,13 @@ struct Knobs {
   int use_pair, pad_small, max_clusters, h_policy, w_policy, sleep_waits, sync_slack, group, demote, quad, gemm_slack;
   int gemm_pol[4];
   int split_correct;
+  int die_groups;
 };
 Knobs knobs() {
   return Knobs{g_use_pair.load(), g_pad_small.load(), g_max_clusters.load(), g_h_policy.load(), g_w_policy.load(),
                g_sleep_waits.load(), g_sync_slack.load(), g_group.load(), g_demote.load(), g_quad.load(),
                g_gemm_slack.load(), {g_gemm_pol[0].load(), g_gemm_pol[1].load(), g_gemm_pol[2].load(),
-                                     g_gemm_pol[3].load()}, g_split_correct.load()};
+                                     g_gemm_pol[3].load()}, g_split_correct.load(), g_die_groups.load()};
 }
 
 tim_status device_info(DevInfo** out) {
@@ -76,6 +83,7 @@ tim_status device_info(DevInfo** out) {
     if (cudaDeviceGetAttribute(&min, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess) return TIM_ERR_CUDA;
     if (cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return TIM_ERR_CUDA;
     d.sm100 = (maj == 10 && min == 0);
+    d.dev_id = dev;
     d.max_pair_clusters = d.num_sms / 2;
     d.max_single_ctas = d.num_sms;
     if (cudaDeviceGetAttribute(&d.l2_bytes, cudaDevAttrL2CacheSize, dev) != cudaSuccess) return TIM_ERR_CUDA;
@@ -83,6 +91,107 @@ tim_status device_info(DevInfo** out) {
   }
   *out = &d;
   return d.sm100 ? TIM_OK : TIM_ERR_UNSUPPORTED;
+}
+
+// SM -> die map of this device, probed once (B200: two dies whose L2 halves each cache what their
+// own SMs read; which SMs sit on which die depends on the chip's floorsweeping).  One CTA per SM
+// times dependent L2 loads of 8 lines 512 KB apart; a line is homed on one die, so its latency
+// splits the SMs into near (~270 cycles) and far (~300) sets.  Per line an Otsu threshold; the
+// lines' patterns are oriented against the clearest one and summed (weighted by agreement), so a
+// few noisy samples cannot flip an SM.  Only the schedule uses the map (which pairs share an
+// M-tile): a wrong bit costs L2 locality, never a result bit.  Skipped while the caller's stream
+// is capturing a graph (allocation and synchronisation are not capturable); tried again later.
+std::mutex g_die_mu;
+static double otsu_threshold(std::vector<double> v, double* sep) {
+  std::sort(v.begin(), v.end());
+  const int n = static_cast<int>(v.size());
+  double tot = 0;
+  for (double x : v) tot += x;
+  double best = -1, thr = v[n / 2], left = 0;
+  for (int k = 1; k < n; ++k) {
+    left += v[k - 1];
+    const double w0 = static_cast<double>(k) / n, w1 = 1.0 - w0;
+    const double m0 = left / k, m1 = (tot - left) / (n - k);
+    const double b = w0 * w1 * (m0 - m1) * (m0 - m1);
+    if (b > best) { best = b; thr = 0.5 * (v[k - 1] + v[k]); }
+  }
+  *sep = best;
+  return thr;
+}
+static void ensure_die_map(DevInfo* d, cudaStream_t caller) {
+  if (d->die_state.load() != 0) return;
+  std::lock_guard<std::mutex> lk(g_die_mu);
+  if (d->die_state.load() != 0) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(caller, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return;
+  }
+  constexpr int kLines = 8, kStride = 65536;  // u64 words between lines (512 KB)
+  const int n = d->num_sms;
+  uint64_t* lines = nullptr;
+  uint32_t *lat = nullptr, *smid = nullptr;
+  cudaStream_t ps = nullptr;
+  std::vector<uint32_t> hl(static_cast<size_t>(n) * kLines), hs(n);
+  bool ok = cudaMalloc(&lines, sizeof(uint64_t) * kLines * kStride) == cudaSuccess &&
+            cudaMalloc(&lat, sizeof(uint32_t) * n * kLines) == cudaSuccess &&
+            cudaMalloc(&smid, sizeof(uint32_t) * n) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaMemsetAsync(lines, 0, sizeof(uint64_t) * kLines * kStride, ps) == cudaSuccess &&
+            launch_die_probe(lines, kLines, kStride, lat, smid, n, ps) == cudaSuccess &&
+            cudaMemcpyAsync(hl.data(), lat, hl.size() * 4, cudaMemcpyDeviceToHost, ps) == cudaSuccess &&
+            cudaMemcpyAsync(hs.data(), smid, hs.size() * 4, cudaMemcpyDeviceToHost, ps) == cudaSuccess &&
+            cudaStreamSynchronize(ps) == cudaSuccess;
+  if (ps) cudaStreamDestroy(ps);
+  cudaFree(lines);
+  cudaFree(lat);
+  cudaFree(smid);
+  cudaGetLastError();
+  // every CTA on its own SM, smid < 256
+  std::vector<int> seen(256, 0);
+  for (int b = 0; ok && b < n; ++b) ok = hs[b] < 256 && !seen[hs[b]]++;
+  if (ok) {
+    std::vector<double> thr(kLines), sep(kLines);
+    std::vector<std::vector<int>> cls(kLines, std::vector<int>(n));
+    int r = 0;
+    for (int l = 0; l < kLines; ++l) {
+      std::vector<double> v(n);
+      for (int b = 0; b < n; ++b) v[b] = hl[b * kLines + l];
+      thr[l] = otsu_threshold(v, &sep[l]);
+      for (int b = 0; b < n; ++b) cls[l][b] = v[b] > thr[l];
+      if (sep[l] > sep[r]) r = l;
+    }
+    std::vector<double> score(n, 0.0);
+    for (int l = 0; l < kLines; ++l) {
+      int agree = 0;
+      for (int b = 0; b < n; ++b) agree += cls[l][b] == cls[r][b];
+      const double a = static_cast<double>(agree) / n;
+      const double w = (a >= 0.5 ? 1.0 : -1.0) * std::fabs(2.0 * a - 1.0);
+      for (int b = 0; b < n; ++b) score[b] += w * (hl[b * kLines + l] - thr[l]);
+    }
+    int n1 = 0;
+    uint64_t mask[4] = {0, 0, 0, 0};
+    for (int b = 0; b < n; ++b)
+      if (score[b] > 0) {
+        ++n1;
+        mask[hs[b] >> 6] |= 1ull << (hs[b] & 63);
+      }
+    ok = n1 >= 0.3 * n && n1 <= 0.7 * n && std::sqrt(sep[r]) >= 5.0;  // two dies, >= ~10 cycles apart
+    if (ok) std::memcpy(d->die_mask, mask, sizeof(mask));
+  }
+  d->die_state.store(ok ? 1 : -1);
+}
+
+// Fill the kernel's die-grouping fields (G > 1, CTA pairs, the whole grid's clusters fit the
+// progress area's spare words).
+static void set_die_grouping(DevInfo* d, LogprobParams& p, int64_t clusters, cudaStream_t s) {
+  p.die_ok = 0;
+  if (p.group <= 1 || clusters + 2 > kMaxProgress || !p.progress) return;
+  ensure_die_map(d, s);
+  if (d->die_state.load() != 1) return;
+  p.die_ok = 1;
+  std::memcpy(p.die_mask, d->die_mask, sizeof(p.die_mask));
+  p.die_counter = p.progress + kMaxProgress - 2;  // zeroed with the progress counters
 }
 
 // ------------------------------------------------------------- tensor maps --
@@ -296,6 +405,7 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   // tiles (one 256-row tile per group) fit in ~75% of L2.  Performance only: which pair runs
   // which (M-tile, slice) unit never changes a row's arithmetic.
   p.group = quad ? 1 : pick_group(dev, pair, p.n_slices, groups, d, kn.group);
+  if (pair && !quad && kn.die_groups) set_die_grouping(dev, p, groups, s);
   if (launch_logprob_fwd(pair, debug_logits != nullptr, sample, quad, th, tw, p, grid, s) != cudaSuccess)
     return TIM_ERR_CUDA;
   if (tp_mode) return TIM_OK;  // the caller all-gathers the slice partials, then tim_logprob_tp_merge
@@ -977,6 +1087,7 @@ static tim_status head_backward_impl(const void* hidden_bf16, int64_t ld_hidden,
     if (kn.max_clusters > 0 && kn.max_clusters < cap) cap = kn.max_clusters;
     const int64_t groups = n_units < cap ? n_units : cap;
     p.group = pick_group(dev, true, S, groups, d, kn.group);
+    if (kn.die_groups) set_die_grouping(dev, p, groups, s);
     CUtensorMap tg;
     if (!encode_g_store(&tg, G, nbc, vocab, g_ld)) return TIM_ERR_CUDA;
     if (launch_head_grad(th, tw, tg, p, static_cast<int>(groups * 2), s) != cudaSuccess) return TIM_ERR_CUDA;
@@ -1217,6 +1328,23 @@ tim_status tim_debug_set_gemm_policy(int32_t dh_a, int32_t dh_b, int32_t dw_a, i
   for (int i = 0; i < 4; ++i)
     if (v[i] < 1 || v[i] > 3) return TIM_ERR_VALUE;
   for (int i = 0; i < 4; ++i) g_gemm_pol[i] = v[i];
+  return TIM_OK;
+}
+
+tim_status tim_debug_set_die_groups(int32_t enable) {
+  if (enable != 0 && enable != 1) return TIM_ERR_VALUE;
+  g_die_groups = enable;
+  return TIM_OK;
+}
+
+tim_status tim_debug_die_map(int32_t* state_out, uint64_t* mask_out4) {
+  if (!state_out || !mask_out4) return TIM_ERR_NULL;
+  DevInfo* dev = nullptr;
+  const tim_status st = device_info(&dev);
+  if (st != TIM_OK) return st;
+  ensure_die_map(dev, nullptr);
+  *state_out = dev->die_state.load();
+  std::memcpy(mask_out4, dev->die_mask, sizeof(dev->die_mask));
   return TIM_OK;
 }
 

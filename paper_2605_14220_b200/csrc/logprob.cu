@@ -329,6 +329,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool leader = prank == 0;
   const uint32_t cid = kPair ? cluster_id_x() : blockIdx.x;
   const uint32_t ncl = kPair ? ncluster_x() : gridDim.x;
+  // Die-aware grouping (G > 1, schedule only -- no row's arithmetic depends on it): the pair takes
+  // a virtual cluster id from its die's end of [0, ncl) -- die 0 counts up from 0, die 1 down from
+  // ncl - 1 -- so consecutive virtual ids, which form the M-tile groups, sit on one die (at most one
+  // group straddles) and each group's H tile lives in one die's L2.  Any die split is a valid
+  // permutation of [0, ncl).  The id goes to both CTAs of the pair through shared::cluster.
+  const bool remap = kPair && kNP == 1 && p.die_ok && p.group > 1;
+  uint32_t* vslot = reinterpret_cast<uint32_t*>(bars + 2 * C::kStages + 4) + 1;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
@@ -346,10 +353,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tmap_w);
   }
   if (warp == 1) tmem_alloc<C::kCtaGroup>(smem_u32(tmem_slot), 512);
+  if (remap && leader && threadIdx.x == 0) {
+    const uint32_t sm = smid_reg();
+    const uint32_t die = static_cast<uint32_t>(p.die_mask[(sm >> 6) & 3] >> (sm & 63)) & 1u;
+    const uint32_t v = die == 0 ? atomicAdd(p.die_counter, 1u) : ncl - 1u - atomicAdd(p.die_counter + 1, 1u);
+    *vslot = v;
+    st_shared_cluster_u32(mapa(smem_u32(vslot), rank ^ 1u), v);
+  }
   tc_fence_before();
   if (kPair) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  const uint32_t vcid = remap ? *vslot : cid;  // the pair's id in the unit schedule
 
   const int n_slices = p.n_slices;
   const int nkb = p.hidden / kBlockK;
@@ -364,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     bool gate = publish;
     uint32_t step = 0, known_min = 0;
     int dm, j;
-    for (int k = 0; sched.unit(cid, k, dm, j); ++k) {
+    for (int k = 0; sched.unit(vcid, k, dm, j); ++k) {
       const int mt = dm * kNP + pid;
       const int m0 = mt * C::kUnitM + prank * kCtaM;
       const int t0 = slice_tile(p, j), t1 = slice_tile(p, j + 1);
@@ -425,11 +440,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
-        if (publish && lane == 0) st_relaxed_gpu(p.progress + cid, step + 1);
+        if (publish && lane == 0) st_relaxed_gpu(p.progress + vcid, step + 1);
       }
       // This CTA has issued its last load of the M-tile (end of its slice range in a full round):
       // demote its H rows from evict_last to evict_normal so dead tiles do not crowd W out of L2.
-      if (p.demote && sched.last_of_mtile(cid, k)) {
+      if (p.demote && sched.last_of_mtile(vcid, k)) {
         const int rows = min(kCtaM, p.n_tok - m0);
         const int lines_per_row = p.hidden / 64;  // 128-B lines of one bf16 row
         const uint8_t* base = static_cast<const uint8_t*>(p.hidden_ptr);
@@ -439,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    if (publish && lane == 0) st_relaxed_gpu(p.progress + cid, 0xFFFFFFFFu);
+    if (publish && lane == 0) st_relaxed_gpu(p.progress + vcid, 0xFFFFFFFFu);
   } else if (warp == 1) {
     // ===================== MMA issuer (the leader CTA's warp 1) =====================
     // The whole warp runs the loop (warp-uniform waits and descriptors); one lane issues each
@@ -454,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t desc_b0 = umma_desc_sw128(smem_u32(smem_b));
       uint32_t stage = 0, phase = 0, acc = 0, aphase = 0;
       int dm, j;
-      for (int k = 0; sched.unit(cid, k, dm, j); ++k) {
+      for (int k = 0; sched.unit(vcid, k, dm, j); ++k) {
         const int t0 = slice_tile(p, j), t1 = slice_tile(p, j + 1);
         for (int vt = t0; vt < t1; ++vt) {
           mbar_wait(smem_u32(&tempty[acc]), aphase ^ 1);
@@ -488,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         kGrad ? ((smem_u32(smem + C::kStages * C::kStageBytes + 256) + 1023u) & ~1023u) + (warp - 2) * 4096u : 0u;
     int gbuf = 0;
     int dm, j;
-    for (int k = 0; sched.unit(cid, k, dm, j); ++k) {
+    for (int k = 0; sched.unit(vcid, k, dm, j); ++k) {
       const int mt = dm * kNP + pid;
       const int row = mt * C::kUnitM + prank * kCtaM + row_in_cta;
       const bool valid = row < p.n_tok;
@@ -751,6 +766,43 @@ cudaError_t launch_logprob_fwd(bool pair, bool debug, bool sample, bool quad, co
                          : launch_fwd<true, false, false, 1>(th, tw, p, grid, stream);
   return debug ? launch_fwd<false, true, false, 1>(th, tw, p, grid, stream)
                : launch_fwd<false, false, false, 1>(th, tw, p, grid, stream);
+}
+
+// One CTA per SM (the caller's shared-memory request keeps a second CTA off every SM): time 32
+// dependent ld.global.cg of each zero-filled line after 4 warm-up loads (the chain's address
+// depends on the loaded value, so nothing overlaps).
+__global__ void __launch_bounds__(32) die_probe_kernel(const uint64_t* lines, int nlines, int stride_u64,
+                                                       uint32_t* lat, uint32_t* smid) {
+  if (threadIdx.x != 0) return;
+  for (int l = 0; l < nlines; ++l) {
+    const uint64_t* line = lines + static_cast<int64_t>(l) * stride_u64;
+    uint64_t v = 0;
+#pragma unroll 1
+    for (int i = 0; i < 4; ++i) {
+      uint64_t x;
+      asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(x) : "l"(line + v));
+      v += x;
+    }
+    const long long t0 = clock64();
+#pragma unroll 1
+    for (int i = 0; i < 32; ++i) {
+      uint64_t x;
+      asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(x) : "l"(line + v));
+      v += x;
+    }
+    const long long t1 = clock64();
+    lat[blockIdx.x * nlines + l] = static_cast<uint32_t>((t1 - t0) / 32) + static_cast<uint32_t>(v);
+  }
+  smid[blockIdx.x] = smid_reg();
+}
+
+cudaError_t launch_die_probe(const uint64_t* lines, int nlines, int stride_u64, uint32_t* lat, uint32_t* smid,
+                             int grid, cudaStream_t stream) {
+  constexpr int kSmem = 160 * 1024;  // more than half of an SM's shared memory: one CTA per SM
+  cudaError_t e = cudaFuncSetAttribute(die_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  if (e != cudaSuccess) return e;
+  die_probe_kernel<<<grid, 32, kSmem, stream>>>(lines, nlines, stride_u64, lat, smid);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_sample_merge(const MergeParams& p, cudaStream_t stream) {

@@ -60,6 +60,11 @@ struct LogprobParams {
   uint16_t* g_out;           // bf16 G block of the current slice, [n_tok][g_ld]
   int64_t g_ld;
   int g_col0;                // first vocab column of the G block
+  // die-aware grouping (G > 1): SM -> die bits from the per-device probe; the pairs of one M-tile
+  // group are taken from the same die so that the group's H tile is not cached in both dies' L2
+  int die_ok;
+  uint64_t die_mask[4];      // bit s = die of SM s (smid < 256)
+  uint32_t* die_counter;     // 2 words in the zeroed workspace header: clusters seen per die
 };
 
 struct MergeParams {
@@ -117,6 +122,10 @@ cudaError_t launch_pad_rows(const void* src, int64_t ld_src_bytes, void* dst, in
 cudaError_t launch_head_grad(const CUtensorMap& th, const CUtensorMap& tw, const CUtensorMap& tg,
                              const LogprobParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_sample_merge(const MergeParams& p, cudaStream_t stream);
+// one-time per-device probe: CTA b runs on SM smid[b] and times dependent L2 loads of `nlines`
+// zero-filled 128-B lines `stride_u64` words apart -> lat[b * nlines + l] (cycles per load)
+cudaError_t launch_die_probe(const uint64_t* lines, int nlines, int stride_u64, uint32_t* lat, uint32_t* smid,
+                             int grid, cudaStream_t stream);
 
 // gemm.cu -- head-backward GEMMs C[m, n] (fp32, row pitch ldc) = A[m, k] B[k, n] (bf16 operands
 // through TMA tensor maps): dH stores, dW accumulates (red.global.add)

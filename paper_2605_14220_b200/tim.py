@@ -110,6 +110,8 @@ _SIGS = {
     "tim_debug_set_cluster": (_I32, [_I32]),
     "tim_debug_set_gemm_slack": (_I32, [_I32]),
     "tim_debug_set_gemm_policy": (_I32, [_I32, _I32, _I32, _I32]),
+    "tim_debug_set_die_groups": (_I32, [_I32]),
+    "tim_debug_die_map": (_I32, [_P, _P]),
     "tim_debug_set_correct_split": (_I32, [_I32]),
 }
 
@@ -518,6 +520,19 @@ def debug_set_gemm_slack(k_blocks: int = 128):
 def debug_set_gemm_policy(dh_a: int = 1, dh_b: int = 1, dw_a: int = 1, dw_b: int = 3):
     """Head-backward GEMM L2 policies (tim_debug_set_gemm_policy); never changes a result bit."""
     _check(lib().tim_debug_set_gemm_policy(int(dh_a), int(dh_b), int(dw_a), int(dw_b)), "tim_debug_set_gemm_policy")
+
+
+def debug_set_die_groups(enable: bool = True):
+    """Die-aware M-tile groups for G > 1 (tim_debug_set_die_groups); never changes a result bit."""
+    _check(lib().tim_debug_set_die_groups(int(bool(enable))), "tim_debug_set_die_groups")
+
+
+def debug_die_map():
+    """(state, [die of SM s for s in 0..255]) from the per-device probe (tim_debug_die_map)."""
+    st = ctypes.c_int32(0)
+    mask = (ctypes.c_uint64 * 4)()
+    _check(lib().tim_debug_die_map(ctypes.byref(st), mask), "tim_debug_die_map")
+    return st.value, [(int(mask[s >> 6]) >> (s & 63)) & 1 for s in range(256)]
 
 
 def debug_set_correct_split(split: bool = True):

@@ -12,6 +12,8 @@ reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 d, V = int(os.environ.get("D", "4096")), 151936
 if os.environ.get("MAXP"):
     tim.debug_set_kernel(True, int(os.environ["MAXP"]))
+if os.environ.get("DIEG") is not None and hasattr(tim, "debug_set_die_groups"):
+    tim.debug_set_die_groups(os.environ["DIEG"] == "1")
 if tun:
     tim.debug_set_tuning(*tun[:4])
     if len(tun) > 4:
