@@ -182,6 +182,16 @@ static void ensure_die_map(DevInfo* d, cudaStream_t caller) {
   d->die_state.store(ok ? 1 : -1);
 }
 
+static void set_gemm_die(DevInfo* d, BwdGemmParams& gp, int max_pairs, cudaStream_t s) {
+  gp.die_ok = 0;
+  if (max_pairs + 2 > kMaxProgress || !gp.progress) return;
+  ensure_die_map(d, s);
+  if (d->die_state.load() != 1) return;
+  gp.die_ok = 1;
+  std::memcpy(gp.die_mask, d->die_mask, sizeof(gp.die_mask));
+  gp.die_counter = gp.progress + kMaxProgress - 2;  // zeroed with the gate counters
+}
+
 // Fill the kernel's die-grouping fields (G > 1, CTA pairs, the whole grid's clusters fit the
 // progress area's spare words).
 static void set_die_grouping(DevInfo* d, LogprobParams& p, int64_t clusters, cudaStream_t s) {
@@ -1103,6 +1113,7 @@ static tim_status head_backward_impl(const void* hidden_bf16, int64_t ld_hidden,
       if (cudaMemsetAsync(prog, 0, kWsHeaderBytes - kWsProgressOffset, s) != cudaSuccess) return TIM_ERR_CUDA;
       BwdGemmParams gp{dhidden_or_null + b0 * d, d, static_cast<int>(nbc), d, vocab, prog, kn.gemm_slack,
                        kn.gemm_pol[0], kn.gemm_pol[1]};
+      if (kn.die_groups) set_gemm_die(dev, gp, max_pairs, s);
       if (launch_bwd_gemm_dh(ta, tb, gp, max_pairs, s) != cudaSuccess) return TIM_ERR_CUDA;
     }
     if (dweight_or_null) {
@@ -1112,6 +1123,7 @@ static tim_status head_backward_impl(const void* hidden_bf16, int64_t ld_hidden,
       if (cudaMemsetAsync(prog, 0, kWsHeaderBytes - kWsProgressOffset, s) != cudaSuccess) return TIM_ERR_CUDA;
       BwdGemmParams gp{dweight_or_null, d, vocab, d, static_cast<int>(nbc), prog, kn.gemm_slack, kn.gemm_pol[2],
                        kn.gemm_pol[3]};
+      if (kn.die_groups) set_gemm_die(dev, gp, max_pairs, s);
       if (launch_bwd_gemm_dw(ta, tb, gp, max_pairs, s) != cudaSuccess) return TIM_ERR_CUDA;
     }
   }

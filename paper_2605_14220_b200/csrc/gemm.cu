@@ -125,6 +125,10 @@ __global__ void __launch_bounds__(kGThreads, 1)
   const bool leader = prank == 0;
   const uint32_t cid = cluster_id_x();
   const uint32_t ncl = ncluster_x();
+  // die-aware virtual cluster ids (the forward kernel's scheme, logprob.cu): consecutive tiles
+  // share an A stream (one M-tile, all N-tiles), so their pairs should share a die's L2
+  const bool remap = p.die_ok != 0;
+  uint32_t* vslot = tmem_slot + 1;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kGStages; ++s) {
@@ -142,10 +146,18 @@ __global__ void __launch_bounds__(kGThreads, 1)
     tma_prefetch(&tmap_b);
   }
   if (warp == 1) tmem_alloc<2>(smem_u32(tmem_slot), 512);
+  if (remap && leader && threadIdx.x == 0) {
+    const uint32_t sm = smid_reg();
+    const uint32_t die = static_cast<uint32_t>(p.die_mask[(sm >> 6) & 3] >> (sm & 63)) & 1u;
+    const uint32_t v = die == 0 ? atomicAdd(p.die_counter, 1u) : ncl - 1u - atomicAdd(p.die_counter + 1, 1u);
+    *vslot = v;
+    st_shared_cluster_u32(mapa(smem_u32(vslot), prank ^ 1u), v);
+  }
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  const uint32_t vcid = remap ? *vslot : cid;
 
   const int n_nt = (p.n + kGTileN - 1) / kGTileN;
   const int n_tiles = ((p.m + 2 * kGCtaM - 1) / (2 * kGCtaM)) * n_nt;
@@ -163,13 +175,13 @@ __global__ void __launch_bounds__(kGThreads, 1)
     const bool publish = prank == 0 && p.sync_slack > 0 && p.progress != nullptr;
     bool gate = publish;
     uint32_t step = 0, known_min = 0;
-    for (int tile = static_cast<int>(cid); tile < n_tiles; tile += static_cast<int>(ncl)) {
+    for (int tile = static_cast<int>(vcid); tile < n_tiles; tile += static_cast<int>(ncl)) {
       const int mt = tile / n_nt, nt = tile % n_nt;
       const int m0 = mt * 2 * kGCtaM + static_cast<int>(prank) * kGCtaM;   // this CTA's A rows
       const int n0 = nt * kGTileN + static_cast<int>(prank) * (kGTileN / 2);  // this CTA's half of B
       for (int kb = 0; kb < nkb; ++kb, ++step) {
         if (gate && (step & 7u) == 0u) {
-          if (lane == 0) st_relaxed_u32(p.progress + cid, step);
+          if (lane == 0) st_relaxed_u32(p.progress + vcid, step);
           if (step > known_min + static_cast<uint32_t>(p.sync_slack)) {
             known_min = gemm_wait_progress(p.progress, ncl, step - p.sync_slack, lane);
             if (known_min + static_cast<uint32_t>(p.sync_slack) < step) gate = false;  // a pair never showed up
@@ -194,7 +206,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
         if (++stage == kGStages) { stage = 0; phase ^= 1; }
       }
     }
-    if (publish && lane == 0) st_relaxed_u32(p.progress + cid, 0xFFFFFFFFu);
+    if (publish && lane == 0) st_relaxed_u32(p.progress + vcid, 0xFFFFFFFFu);
   } else if (warp == 1) {
     // ===================== MMA issuer (the leader CTA's warp 1) =====================
     if (leader) {
@@ -206,7 +218,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
       constexpr uint32_t kAStep = kAMN ? 128u : 2u;
       constexpr uint32_t kBStep = 128u;
       uint32_t stage = 0, phase = 0, acc = 0, aphase = 0;
-      for (int tile = static_cast<int>(cid); tile < n_tiles; tile += static_cast<int>(ncl)) {
+      for (int tile = static_cast<int>(vcid); tile < n_tiles; tile += static_cast<int>(ncl)) {
         mbar_wait(smem_u32(&tempty[acc]), aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kGTileN;
@@ -232,7 +244,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
     const int row_in_cta = q * 32 + lane;
     const uint32_t tempty_leader = mapa(smem_u32(tempty), 0);
     uint32_t acc = 0, aphase = 0;
-    for (int tile = static_cast<int>(cid); tile < n_tiles; tile += static_cast<int>(ncl)) {
+    for (int tile = static_cast<int>(vcid); tile < n_tiles; tile += static_cast<int>(ncl)) {
       const int mt = tile / n_nt, nt = tile % n_nt;
       const int row = mt * 2 * kGCtaM + static_cast<int>(prank) * kGCtaM + row_in_cta;
       const bool valid = row < p.m;

@@ -136,6 +136,10 @@ struct BwdGemmParams {
   uint32_t* progress;  // [pairs] k-blocks issued per CTA pair (zeroed per launch), or null: no gate
   int sync_slack;      // max k-blocks a pair may run ahead of the slowest (0 = no gate)
   int a_policy, b_policy;  // L2 policy of the A / B tile loads: 1 normal, 2 evict_first, 3 evict_last
+  // die-aware tile order (as LogprobParams): the pairs sharing an operand stream sit on one die
+  int die_ok;
+  uint64_t die_mask[4];
+  uint32_t* die_counter;
 };
 cudaError_t launch_bwd_gemm_dh(const CUtensorMap& tg_kmajor, const CUtensorMap& tw_mn, const BwdGemmParams& p,
                                int max_pairs, cudaStream_t stream);
