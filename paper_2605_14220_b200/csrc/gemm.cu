@@ -150,14 +150,14 @@ __global__ void __launch_bounds__(kGThreads, 1)
     const uint32_t sm = smid_reg();
     const uint32_t die = static_cast<uint32_t>(p.die_mask[(sm >> 6) & 3] >> (sm & 63)) & 1u;
     const uint32_t v = die == 0 ? atomicAdd(p.die_counter, 1u) : ncl - 1u - atomicAdd(p.die_counter + 1, 1u);
-    *vslot = v;
-    st_shared_cluster_u32(mapa(smem_u32(vslot), prank ^ 1u), v);
+    *vslot = v;  // the peer CTA reads it through shared::cluster after the cluster barrier
   }
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const uint32_t vcid = remap ? *vslot : cid;
+  const uint32_t vcid =
+      !remap ? cid : (leader ? *vslot : ld_shared_cluster_u32(mapa(smem_u32(vslot), cluster_ctarank() & ~1u)));
 
   const int n_nt = (p.n + kGTileN - 1) / kGTileN;
   const int n_tiles = ((p.m + 2 * kGCtaM - 1) / (2 * kGCtaM)) * n_nt;

@@ -357,14 +357,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t sm = smid_reg();
     const uint32_t die = static_cast<uint32_t>(p.die_mask[(sm >> 6) & 3] >> (sm & 63)) & 1u;
     const uint32_t v = die == 0 ? atomicAdd(p.die_counter, 1u) : ncl - 1u - atomicAdd(p.die_counter + 1, 1u);
-    *vslot = v;
-    st_shared_cluster_u32(mapa(smem_u32(vslot), rank ^ 1u), v);
+    *vslot = v;  // the peer CTA reads it through shared::cluster after the cluster barrier
   }
   tc_fence_before();
   if (kPair) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const uint32_t vcid = remap ? *vslot : cid;  // the pair's id in the unit schedule
+  // the pair's id in the unit schedule: the leader CTA's slot (a DSMEM read, after the barrier
+  // that guarantees the peer CTA has started and the leader's write is visible)
+  const uint32_t vcid = !remap ? cid : (leader ? *vslot : ld_shared_cluster_u32(mapa(smem_u32(vslot), pl)));
 
   const int n_slices = p.n_slices;
   const int nkb = p.hidden / kBlockK;

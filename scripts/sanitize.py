@@ -36,3 +36,23 @@ res2 = tim.correct(num2, den2, cu2, tim.PRESETS["tis-srs-k3-corr-ratio"], mask2)
 pp2 = tim.ppo_loss(num2, den2, torch.randn(n2, device=dev), cu2, tim.PPOConfig(), coeff=res2["coeff"])
 torch.cuda.synchronize()
 print("sanitize large run ok", n2, res2["stats"]["n_seq_rejected"], pp2["stats"]["n_clipped"])
+# round 2: the fused one-launch correction (grid barriers), the d = 4096 head with die-aware
+# M-tile groups (G = 2, the per-device die probe, shared::cluster id exchange), the TP head's
+# library collective on a 1-rank communicator
+tim.debug_set_correct_split(False)
+res3 = tim.correct(num2, den2, cu2, tim.PRESETS["tis-srs-k3-corr-ratio"], mask2)
+tim.debug_set_correct_split(True)
+W4 = synth.head_weight(151936, 4096, 2, device=dev)
+ids4 = synth.token_ids(600, 151936, 2, device=dev)
+H4 = synth.hidden_states(600, 4096, 2, device=dev, weight=W4, ids=ids4, mode="peaked")
+lp4, _ = tim.logprob(H4, W4, ids4)
+import torch.distributed as dist
+os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+os.environ.setdefault("MASTER_PORT", "29541")
+dist.init_process_group("gloo", rank=0, world_size=1)
+comm = tim.Comm()
+lpt, _ = tim.logprob_tp(H, W, 1000, ids, comm)
+comm.close()
+dist.destroy_process_group()
+torch.cuda.synchronize()
+print("sanitize round-2 run ok", int(res3["stats"]["n_seq_rejected"]), float(lp4.sum()), bool(torch.equal(lpt, lp)))
