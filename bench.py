@@ -44,6 +44,7 @@ import synth  # noqa: E402
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 KERNELS_PER_STEP = 5  # logprob fwd + merge, correct local + finish + zero
+_SMS = 148            # B200 SMs (the clock-peak figure below; the kernels query the device themselves)
 
 
 def _peaks():
@@ -118,6 +119,22 @@ def _ncu_tensor_pct(config: str):
         if v is None and config == "c1":
             v = d["metrics"]["sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"][0]
         return None if v is None else float(v)
+    except Exception:
+        return None
+
+
+def _kernel_clock_mhz(tim, dev):
+    """Average SM clock of the last tim_logprob launch on this stream, measured inside the kernel
+    (CTA 0: clock64 and globaltimer at its start and end, workspace header reserved[1..4]) -- the
+    clock the power cap actually sustained, which nvidia-smi's 200-ms samples can overstate."""
+    try:
+        key = (str(dev), torch.cuda.current_stream(dev).cuda_stream, "logprob")
+        ws = tim._ws_cache.get(key)
+        if ws is None:
+            return None
+        h = ws[:64].view(torch.int64).cpu().tolist()  # WsHeader: bad_inv, counter|pad, reserved[0..5]
+        cyc, ns = h[5] - h[3], h[6] - h[4]            # clk = reserved[1..4]: {cyc0, ns0, cyc1, ns1}
+        return round(cyc / ns * 1e3, 1) if ns > 0 and cyc > 0 else None
     except Exception:
         return None
 
@@ -279,6 +296,7 @@ def measure(tim, cfg, args, world, rank, local, dev, comm, steps, warmup, full):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     clk = clocks.stop()
+    clk["sm_mhz_in_kernel"] = _kernel_clock_mhz(tim, dev)
     ms = t0.elapsed_time(t1)
     lp_ms = sum(a.elapsed_time(b) for a, b in evs) / steps
     if world > 1:
@@ -340,7 +358,12 @@ def measure(tim, cfg, args, world, rank, local, dev, comm, steps, warmup, full):
                      "ncu_tensor_pipe_pct": _ncu_tensor_pct(cfg.name),
                      "kernel": "tim_logprob (tcgen05 GEMM + fused epilogue + slice merge)",
                      "kernel_ms": lp_ms, "algorithmic_flop_per_token": 2 * cfg.vocab * cfg.hidden,
-                     "tokens_per_launch": N},
+                     "tokens_per_launch": N,
+                     # the tensor pipe's peak at the clock the kernel actually ran at (in-kernel
+                     # clock64 / globaltimer): 148 SMs x 8192 dense bf16 flop per SM-cycle (from ncu:
+                     # flops / tensor-active cycles); frac_of_clock_peak = what the power cap leaves
+                     "frac_of_clock_peak": (achieved / (_SMS * 8192 * clk["sm_mhz_in_kernel"] * 1e-6))
+                     if clk.get("sm_mhz_in_kernel") else None},
         "clocks": clk,
         "correction_stats": {k: stats[k] for k in ("n_resp_tok", "n_truncated", "n_seq_rejected", "max_abs_delta",
                                                      "mean_abs_delta", "mean_k3")},

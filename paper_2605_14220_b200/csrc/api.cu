@@ -403,6 +403,7 @@ tim_status logprob_impl(const void* hidden, int64_t ld_hidden, const void* weigh
   p.ld_hidden_bytes = h_ld * 2;
   p.demote = kn.demote;
   p.gate_stats = &hdr->reserved[5];  // read back by the diagnostics scripts (zeroed with the header)
+  p.clk = &hdr->reserved[1];         // reserved[1..4]: SM clock inside the kernel (bench.py reads it)
   p.row_keys = row_keys;
   p.seed = seed;
   p.partials2 = sample ? partials + static_cast<size_t>(vocab_slices(vocab)) * static_cast<size_t>(n_tok) : nullptr;

@@ -327,6 +327,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t pid = rank >> 1;        // pair inside the cluster
   const uint32_t pl = rank & ~1u;        // rank of this pair's leader CTA
   const bool leader = prank == 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && p.clk) {  // the SM clock actually sustained (diagnostics)
+    p.clk[0] = static_cast<unsigned long long>(clock64());
+    p.clk[1] = globaltimer_ns();
+  }
   const uint32_t cid = kPair ? cluster_id_x() : blockIdx.x;
   const uint32_t ncl = kPair ? ncluster_x() : gridDim.x;
   // Die-aware grouping (G > 1, schedule only -- no row's arithmetic depends on it): the pair takes
@@ -616,6 +620,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
+  if (blockIdx.x == 0 && threadIdx.x == 0 && p.clk) {
+    p.clk[2] = static_cast<unsigned long long>(clock64());
+    p.clk[3] = globaltimer_ns();
+  }
   if (kGrad && warp >= 2 && lane == 0) bulk_wait_group_all();  // the G tiles are written
   __syncwarp();
   tc_fence_before();

@@ -52,6 +52,7 @@ struct LogprobParams {
   int64_t ld_hidden_bytes;
   int demote;                // demote finished H tiles to evict_normal
   unsigned long long* gate_stats;  // diagnostics: number of progress gates given up (timed out)
+  unsigned long long* clk;         // diagnostics: {clock64, globaltimer} at CTA 0's start and end
   // head backward (NEXT-3) gradient epilogue
   const float* grad_logp;    // [n_tok] dL/dlogp
   const float* grad_ent;     // [n_tok] dL/dH or null
