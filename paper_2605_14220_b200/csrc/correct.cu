@@ -79,14 +79,6 @@ __device__ __forceinline__ Chunk load_chunk(const LocalParams& p, long long i0) 
   return c;
 }
 
-__device__ __forceinline__ Chunk load_vec(const LocalParams& p, long long i0) {
-  Chunk c;
-  c.num = __ldcs(reinterpret_cast<const float4*>(p.num + i0));
-  c.den = __ldcs(reinterpret_cast<const float4*>(p.den + i0));
-  c.resp = p.resp ? __ldcs(reinterpret_cast<const unsigned int*>(p.resp + i0)) : 0x01010101u;
-  return c;
-}
-
 __device__ __forceinline__ void store_chunk(const LocalParams& p, long long i0, bool full, const float* w_out,
                                             const float* c_out, uint32_t kbits) {
   if (full) {
@@ -123,17 +115,15 @@ struct FastAcc {
   unsigned resp, trunc, rej, seq_t;
 };
 
-// One chunk (four tokens per lane), the short contract polynomials for every token with
-// |delta| <= 2^-6 in lock-step.  kMasked = false: the warp-uniform common case -- every token
-// small, no sequence boundary inside any lane's tokens, the response mask all-1 (sum_on) or
-// all-0 over the chunk; no per-token selects.  kMasked = true: per-token masks, and the slow
-// tokens (larger or non-finite delta, partial chunk, sequence boundary) then take the full
-// contract per lane with int128 sums and the sequence walk in the lane's shared-memory state.
-template <bool kMasked, bool kOut, int kSeqK, bool kTis, bool kTokRs>
-__device__ __forceinline__ void chunk_body(const LocalParams& p, LaneState& st, FastAcc& fa, const float4 numv,
-                                           const float4 denv, const uint32_t resp_bits, const long long i0,
-                                           const bool full, const bool lane_whole, const bool sum_on,
-                                           const double (&dv)[kTpl]) {
+// A chunk that the fast body cannot take (a sequence or prompt / response boundary inside it, a
+// partial or unaligned chunk, a non-interior configuration): per-token response masks, the short
+// contract series in lock-step for every token with |delta| <= 2^-6 of a whole lane (four tokens
+// before the lane's next sequence boundary), and the remaining (slow) tokens afterwards with the
+// full contract per lane, int128 sums and the sequence walk in the lane's shared-memory state.
+template <bool kOut, int kSeqK, bool kTis, bool kTokRs>
+__device__ __forceinline__ void masked_body(const LocalParams& p, LaneState& st, FastAcc& fa, const uint32_t resp_bits,
+                                            const long long i0, const bool full, const bool lane_whole,
+                                            const double (&dv)[kTpl]) {
   constexpr bool kSeq = kSeqK != TIM_SEQ_NONE;
   constexpr bool seq_k1 = kSeqK == TIM_SEQ_K1;
   const CorrectDevCfg& cfg = p.cfg;
@@ -142,15 +132,11 @@ __device__ __forceinline__ void chunk_body(const LocalParams& p, LaneState& st, 
   double ds[kTpl], k3s[kTpl];
 #pragma unroll
   for (int k = 0; k < kTpl; ++k) {
-    if (kMasked) {
-      const bool sm = fabs(dv[k]) <= kSmall;  // false for NaN / inf
-      if (!sm || !lane_whole) slow |= 1u << k;
-      ds[k] = sm ? dv[k] : 0.0;  // slow small tokens reuse their k3s
-    } else {
-      ds[k] = dv[k];
-    }
+    const bool sm = fabs(dv[k]) <= kSmall;  // false for NaN / inf
+    if (!sm || !lane_whole) slow |= 1u << k;
+    ds[k] = sm ? dv[k] : 0.0;  // slow small tokens reuse their k3s
   }
-  if (kMasked || kTis || sum_on) {  // short K3 series, four independent Horner chains
+  {  // short K3 series, four independent Horner chains
     double q[kTpl];
 #pragma unroll
     for (int k = 0; k < kTpl; ++k) q[k] = kInvFact[9];
@@ -168,8 +154,8 @@ __device__ __forceinline__ void chunk_body(const LocalParams& p, LaneState& st, 
 #pragma unroll
   for (int k = 0; k < kTpl; ++k) {
     const double d = ds[k];
-    const bool resp = kMasked ? ((resp_bits >> (8 * k)) & 0xffu) != 0u : sum_on;
-    const bool use = kMasked ? (resp && !((slow >> k) & 1u)) : sum_on;
+    const bool resp = ((resp_bits >> (8 * k)) & 0xffu) != 0u;
+    const bool use = resp && !((slow >> k) & 1u);
     bool trunc = false;
     float w = 1.f;
     if (kTis) {  // (float) min(e, cap) == min((float) e, (float) cap): rounding is monotonic
@@ -180,49 +166,41 @@ __device__ __forceinline__ void chunk_body(const LocalParams& p, LaneState& st, 
     w_out[k] = w;
     c_out[k] = (resp && keep) ? w : 0.f;
     kbits |= static_cast<uint32_t>(keep) << (8 * k);
-    if (kMasked || sum_on) {
-      const double dz = kMasked ? (use ? d : 0.0) : d;  // unused tokens add exactly 0
-      const double kz = kMasked ? (use ? k3s[k] : 0.0) : k3s[k];
-      const double x1 = rint(__dmul_rn(-dz, kTwo52));  // exact scaling, then round to integer
-      const double x3 = rint(__dmul_rn(kz, kTwo52));
-      fa.k1 = __dadd_rn(fa.k1, x1);
-      fa.k3 = __dadd_rn(fa.k3, x3);
-      fa.ab = __dadd_rn(fa.ab, fabs(x1));
-      cmx = fabs(dz) > cmx ? fabs(dz) : cmx;
-      if (kMasked) cn += use ? 1u : 0u;
-      if (kTis) ctr += (use && trunc) ? 1u : 0u;
-      if (kTokRs) crj += (use && !keep) ? 1u : 0u;
-      if (kSeq) {
-        const double xq = seq_k1 ? x1 : x3;
-        if (kTokRs) {
-          fa.seq = __dadd_rn(fa.seq, keep ? xq : 0.0);
-          cst += (use && keep) ? 1u : 0u;
-        } else {
-          fa.seq = __dadd_rn(fa.seq, xq);
-          if (kMasked) cst += use ? 1u : 0u;
-        }
+    const double dz = use ? d : 0.0;  // unused tokens add exactly 0
+    const double kz = use ? k3s[k] : 0.0;
+    const double x1 = rint(__dmul_rn(-dz, kTwo52));  // exact scaling, then round to integer
+    const double x3 = rint(__dmul_rn(kz, kTwo52));
+    fa.k1 = __dadd_rn(fa.k1, x1);
+    fa.k3 = __dadd_rn(fa.k3, x3);
+    fa.ab = __dadd_rn(fa.ab, fabs(x1));
+    cmx = fabs(dz) > cmx ? fabs(dz) : cmx;
+    cn += use ? 1u : 0u;
+    if (kTis) ctr += (use && trunc) ? 1u : 0u;
+    if (kTokRs) crj += (use && !keep) ? 1u : 0u;
+    if (kSeq) {
+      const double xq = seq_k1 ? x1 : x3;
+      if (kTokRs) {
+        fa.seq = __dadd_rn(fa.seq, keep ? xq : 0.0);
+        cst += (use && keep) ? 1u : 0u;
+      } else {
+        fa.seq = __dadd_rn(fa.seq, xq);
+        cst += use ? 1u : 0u;
       }
     }
   }
-  if (kMasked || sum_on) {
-    fa.mx = cmx > fa.mx ? cmx : fa.mx;
-    fa.resp += kMasked ? cn : kTpl;
-    fa.trunc += ctr;
-    fa.rej += crj;
-    if (kSeq) fa.seq_t += (kMasked || kTokRs) ? cst : kTpl;
-  }
+  fa.mx = cmx > fa.mx ? cmx : fa.mx;
+  fa.resp += cn;
+  fa.trunc += ctr;
+  fa.rej += crj;
+  if (kSeq) fa.seq_t += cst;
 
-  if (kMasked && slow) {  // rare: the full contract per token, in the slow tokens' lanes only
+  if (slow) {  // rare: the full contract per token, in the slow tokens' lanes only
     if (kSeq) {  // the lane may leave its sequence below: its pending sums go with it
       st.seq_x += __double2ll_rn(fa.seq);
       st.seq_t += fa.seq_t;
       fa.seq = 0.0;
       fa.seq_t = 0;
     }
-    const float num[4] = {numv.x, numv.y, numv.z, numv.w};
-    const float den[4] = {denv.x, denv.y, denv.z, denv.w};
-    (void)num;
-    (void)den;
 #pragma unroll
     for (int k = 0; k < kTpl; ++k) {
       if (!((slow >> k) & 1u)) continue;
@@ -568,7 +546,7 @@ __device__ __forceinline__ void pass1_body(const LocalParams& p) {
       fast_body<kOut, kSeqK, kTis, kTokRs>(p, st, fa, i0, f_all, dv);
     } else {
       const bool lane_whole = !(kSeq && p.tok_begin + i0 + (kTpl - 1) >= st.next_b);
-      chunk_body<true, kOut, kSeqK, kTis, kTokRs>(p, st, fa, numv, denv, resp, i0, true, lane_whole, true, dv);
+      masked_body<kOut, kSeqK, kTis, kTokRs>(p, st, fa, resp, i0, true, lane_whole, dv);
       if (kSeq && p.interior) {  // back onto one cursor: lane 31 holds the furthest sequence
         const long long ms = __shfl_sync(0xffffffffu, st.sid, 31);
         if (__any_sync(0xffffffffu, st.sid != ms)) {
@@ -597,7 +575,7 @@ __device__ __forceinline__ void pass1_body(const LocalParams& p) {
     dv[2] = __dsub_rn(static_cast<double>(cc.num.z), static_cast<double>(cc.den.z));
     dv[3] = __dsub_rn(static_cast<double>(cc.num.w), static_cast<double>(cc.den.w));
     const bool lane_whole = full && !(kSeq && p.tok_begin + i0 + (kTpl - 1) >= st.next_b);
-    chunk_body<true, kOut, kSeqK, kTis, kTokRs>(p, st, fa, cc.num, cc.den, cc.resp, i0, full, lane_whole, true, dv);
+    masked_body<kOut, kSeqK, kTis, kTokRs>(p, st, fa, cc.resp, i0, full, lane_whole, dv);
     fold();
   }
   fold();
