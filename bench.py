@@ -297,6 +297,11 @@ def measure(tim, cfg, args, world, rank, local, dev, comm, steps, warmup, full):
     torch.cuda.synchronize()
     clk = clocks.stop()
     clk["sm_mhz_in_kernel"] = _kernel_clock_mhz(tim, dev)
+    try:  # the SM -> die map behind the die-aware M-tile groups (state 1 = probed and valid)
+        st_dm, die = tim.debug_die_map()
+        clk["die_map"] = {"state": st_dm, "die1_sms": int(sum(die))}
+    except Exception:
+        pass
     ms = t0.elapsed_time(t1)
     lp_ms = sum(a.elapsed_time(b) for a, b in evs) / steps
     if world > 1:

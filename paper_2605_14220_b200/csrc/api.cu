@@ -95,7 +95,7 @@ tim_status device_info(DevInfo** out) {
 
 // SM -> die map of this device, probed once (B200: two dies whose L2 halves each cache what their
 // own SMs read; which SMs sit on which die depends on the chip's floorsweeping).  One CTA per SM
-// times dependent L2 loads of 8 lines 512 KB apart; a line is homed on one die, so its latency
+// times dependent L2 loads of 16 lines 512 KB apart; a line is homed on one die, so its latency
 // splits the SMs into near (~270 cycles) and far (~300) sets.  Per line an Otsu threshold; the
 // lines' patterns are oriented against the clearest one and summed (weighted by agreement), so a
 // few noisy samples cannot flip an SM.  Only the schedule uses the map (which pairs share an
@@ -127,7 +127,7 @@ static void ensure_die_map(DevInfo* d, cudaStream_t caller) {
     cudaGetLastError();
     return;
   }
-  constexpr int kLines = 8, kStride = 65536;  // u64 words between lines (512 KB)
+  constexpr int kLines = 16, kStride = 65536;  // u64 words between lines (512 KB)
   const int n = d->num_sms;
   uint64_t* lines = nullptr;
   uint32_t *lat = nullptr, *smid = nullptr;
@@ -169,14 +169,32 @@ static void ensure_die_map(DevInfo* d, cudaStream_t caller) {
       const double w = (a >= 0.5 ? 1.0 : -1.0) * std::fabs(2.0 * a - 1.0);
       for (int b = 0; b < n; ++b) score[b] += w * (hl[b * kLines + l] - thr[l]);
     }
-    int n1 = 0;
+    // the two SMs of a TPC (smid 2k, 2k + 1: where a CTA pair lands) share a die -- pool their
+    // scores, and refuse the map when too many pairs disagree (a noisy probe must not group worse
+    // than the cluster-id order does)
+    std::vector<double> by_smid(256, 0.0);
+    std::vector<int> have(256, 0);
+    for (int b = 0; b < n; ++b) {
+      by_smid[hs[b]] = score[b];
+      have[hs[b]] = 1;
+    }
+    int n1 = 0, pairs = 0, disagree = 0;
     uint64_t mask[4] = {0, 0, 0, 0};
-    for (int b = 0; b < n; ++b)
-      if (score[b] > 0) {
-        ++n1;
-        mask[hs[b] >> 6] |= 1ull << (hs[b] & 63);
+    for (int s0 = 0; s0 < 256; s0 += 2) {
+      if (!have[s0] && !have[s0 + 1]) continue;
+      const double t = by_smid[s0] + by_smid[s0 + 1];
+      if (have[s0] && have[s0 + 1]) {
+        ++pairs;
+        disagree += (by_smid[s0] > 0) != (by_smid[s0 + 1] > 0);
       }
-    ok = n1 >= 0.3 * n && n1 <= 0.7 * n && std::sqrt(sep[r]) >= 5.0;  // two dies, >= ~10 cycles apart
+      for (int k = 0; k < 2; ++k)
+        if (have[s0 + k] && t > 0) {
+          ++n1;
+          mask[(s0 + k) >> 6] |= 1ull << ((s0 + k) & 63);
+        }
+    }
+    ok = n1 >= 0.3 * n && n1 <= 0.7 * n && std::sqrt(sep[r]) >= 5.0 &&  // two dies, >= ~10 cycles apart
+         disagree * 10 <= pairs;                                           // <= 10% of TPCs split
     if (ok) std::memcpy(d->die_mask, mask, sizeof(mask));
   }
   d->die_state.store(ok ? 1 : -1);

@@ -777,7 +777,7 @@ cudaError_t launch_logprob_fwd(bool pair, bool debug, bool sample, bool quad, co
                : launch_fwd<false, false, false, 1>(th, tw, p, grid, stream);
 }
 
-// One CTA per SM (the caller's shared-memory request keeps a second CTA off every SM): time 32
+// One CTA per SM (the caller's shared-memory request keeps a second CTA off every SM): time 64
 // dependent ld.global.cg of each zero-filled line after 4 warm-up loads (the chain's address
 // depends on the loaded value, so nothing overlaps).
 __global__ void __launch_bounds__(32) die_probe_kernel(const uint64_t* lines, int nlines, int stride_u64,
@@ -794,13 +794,13 @@ __global__ void __launch_bounds__(32) die_probe_kernel(const uint64_t* lines, in
     }
     const long long t0 = clock64();
 #pragma unroll 1
-    for (int i = 0; i < 32; ++i) {
+    for (int i = 0; i < 64; ++i) {
       uint64_t x;
       asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(x) : "l"(line + v));
       v += x;
     }
     const long long t1 = clock64();
-    lat[blockIdx.x * nlines + l] = static_cast<uint32_t>((t1 - t0) / 32) + static_cast<uint32_t>(v);
+    lat[blockIdx.x * nlines + l] = static_cast<uint32_t>((t1 - t0) / 64) + static_cast<uint32_t>(v);
   }
   smid[blockIdx.x] = smid_reg();
 }
