@@ -1224,6 +1224,7 @@ tim_status tim_ppo_local(const float* cur, const float* old, const float* adv, c
   p.hist_lo = cfg->hist_lo;
   p.hist_inv_width = cfg->hist_inv_width;
   p.bins = cfg->hist_bins;
+  p.bins_d = static_cast<double>(cfg->hist_bins);
   p.loss = loss;
   p.grad = grad;
   p.clipped = clipped;

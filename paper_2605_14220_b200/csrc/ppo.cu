@@ -13,6 +13,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <type_traits>
 
 #include "contract.cuh"
 #include "ptx.cuh"
@@ -36,21 +37,27 @@ constexpr int kPpoStageBytes = 4 * 512;     // cur, old, adv, coeff (or the u8 m
 constexpr int kPpoThreads = TIM_PPO_THREADS;
 constexpr int kPpoMinB = TIM_PPO_MINB;
 constexpr int kMaxHistBins = 1024;
+constexpr long long kPpoFold = 1024;       // chunks per int64 K1 / K3 fold: 2^10 x 2^52 < 2^63
 constexpr double kPpoFastLoss = 256.0;      // fast path: |loss| <= 2^8, so |X| <= 2^60 and four fit int64
 
 struct PpoChunk {
   float4 cur, old, adv, w;  // w = coeff, or the response mask as 0 / 1
 };
 
+// Weight source, a kernel template argument (no per-chunk pointer tests): the correction
+// coefficient, the u8 response mask, or none (every token weight 1).
+enum PpoWeight : int { kWCoeff = 0, kWResp = 1, kWNone = 2 };
+
+template <int kW>
 __device__ __forceinline__ PpoChunk ppo_load(const PpoLocalParams& p, long long i0) {
   PpoChunk c;
   if (p.vec && i0 + kPpoTpl <= p.n) {
     c.cur = __ldcs(reinterpret_cast<const float4*>(p.cur + i0));
     c.old = __ldcs(reinterpret_cast<const float4*>(p.old + i0));
     c.adv = __ldcs(reinterpret_cast<const float4*>(p.adv + i0));
-    if (p.coeff) {
+    if (kW == kWCoeff) {
       c.w = __ldcs(reinterpret_cast<const float4*>(p.coeff + i0));
-    } else if (p.resp) {
+    } else if (kW == kWResp) {
       const uint32_t m = __ldcs(reinterpret_cast<const unsigned int*>(p.resp + i0));
       c.w = make_float4((m & 0xffu) ? 1.f : 0.f, (m & 0xff00u) ? 1.f : 0.f, (m & 0xff0000u) ? 1.f : 0.f,
                         (m & 0xff000000u) ? 1.f : 0.f);
@@ -66,7 +73,7 @@ __device__ __forceinline__ PpoChunk ppo_load(const PpoLocalParams& p, long long 
       v[0][k] = in ? p.cur[i] : 0.f;
       v[1][k] = in ? p.old[i] : 0.f;
       v[2][k] = in ? p.adv[i] : 0.f;
-      v[3][k] = !in ? 0.f : (p.coeff ? p.coeff[i] : ((p.resp ? p.resp[i] != 0 : true) ? 1.f : 0.f));
+      v[3][k] = !in ? 0.f : (kW == kWCoeff ? p.coeff[i] : ((kW == kWResp ? p.resp[i] != 0 : true) ? 1.f : 0.f));
     }
     c.cur = make_float4(v[0][0], v[0][1], v[0][2], v[0][3]);
     c.old = make_float4(v[1][0], v[1][1], v[1][2], v[1][3]);
@@ -76,15 +83,30 @@ __device__ __forceinline__ PpoChunk ppo_load(const PpoLocalParams& p, long long 
   return c;
 }
 
-// dynamic shared memory: [2][bins + 2] int histogram, then the per-warp rings (16-B aligned)
+// dynamic shared memory: [2][bins + 2] int histogram, 32 per-lane sink slots (the lock-step path's
+// atomics for A = 0 tokens land there, so the atomic needs no branch), then the per-warp rings
+// (16-B aligned)
 __host__ __device__ constexpr size_t ppo_hist_bytes(int bins) {
-  return (sizeof(int) * 2 * static_cast<size_t>(bins + 2) + 15) & ~size_t(15);
+  return (sizeof(int) * (2 * static_cast<size_t>(bins + 2) + 32) + 15) & ~size_t(15);
 }
 
+// Slot of C(r) = -(r - 1) A: 0 below hist_lo, bins + 1 at or above the top edge, else floor + 1.
+// Branch-free: clamping the saturated integer floor to [-1, bins] gives the same slot for every
+// non-NaN C (C is never NaN for a counted token: r is finite or +inf, A finite and nonzero).
 __device__ __forceinline__ int hist_slot(const PpoLocalParams& p, double r, double A) {
   const double C = __dmul_rn(-__dsub_rn(r, 1.0), A);
-  const double raw = floor(__dmul_rn(__dsub_rn(C, p.hist_lo), p.hist_inv_width));
-  return raw < 0.0 ? 0 : (raw >= static_cast<double>(p.bins) ? p.bins + 1 : static_cast<int>(raw) + 1);
+  // floor and convert in one (cvt.rmi.s32.f64 saturates out-of-range values and infinities)
+  const int raw = __double2int_rd(__dmul_rn(__dsub_rn(C, p.hist_lo), p.hist_inv_width));
+  return min(max(raw, -1), p.bins) + 1;
+}
+
+// loss = -(w * (clipped ? clip * A : r * A)): one product of the selected factor, bit-identical
+__device__ __forceinline__ double ppo_token_loss(const PpoLocalParams& p, double r, double A, float w,
+                                                 bool& clipped) {
+  const bool pos = A > 0.0;
+  clipped = (pos & (r > p.clip_hi)) | ((A < 0.0) & (r < p.clip_lo));  // no short-circuit branch
+  const double f = clipped ? (pos ? p.clip_hi : p.clip_lo) : r;
+  return -__dmul_rn(static_cast<double>(w), __dmul_rn(f, A));
 }
 
 // 4 tokens per lane, next chunk prefetched, a lock-step fast path (|delta| <= 2^-2, |loss| <=
@@ -92,6 +114,7 @@ __device__ __forceinline__ int hist_slot(const PpoLocalParams& p, double r, doub
 // folded into int128 per chunk) and a rare per-lane slow path with the full contract (larger delta
 // or loss, non-finite input, partial or unaligned chunk, sequence boundary inside the lane's
 // tokens).
+template <int kW>
 __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLocalParams p) {
   extern __shared__ __align__(16) int sh_hist[];  // [2][bins + 2], then the rings
   const int nslot = p.bins + 2;
@@ -107,7 +130,17 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
   const long long c_end = c_begin + cpw < n_chunks ? c_begin + cpw : n_chunks;
 
   unsigned c_contrib = 0, c_clip = 0, c_zero = 0, c_sat = 0;
+  // s_loss collects each flushed sequence segment (acc.x), so the hot path adds the chunk's loss
+  // once (to acc.x); the lock-step path's K1 / K3 chunk sums (|X| <= 2^52 per chunk) go to int64
+  // lane accumulators folded into the int128 sums every kPpoFold chunks.
   __int128 s_loss = 0, s_k1 = 0, s_k3 = 0;
+  long long f_k1 = 0, f_k3 = 0;
+  auto fold = [&]() {
+    s_k1 += f_k1;
+    s_k3 += f_k3;
+    f_k1 = 0;
+    f_k3 = 0;
+  };
   unsigned long long bad_inv = 0;
 
   SeqAcc acc;
@@ -123,16 +156,19 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
 
   if (blockIdx.x == 0 && threadIdx.x == 0) shard_range_check(p.cu, p.n_seq, p.tok_begin, p.n, bad_inv);
 
-  auto body = [&](const PpoChunk& cur, const long long i0) {
+  // kFull: a whole vector chunk (the ring loop) -- known at compile time there
+  auto body = [&](const PpoChunk& cur, const long long i0, auto full_tag) {
     const float cu_[4] = {cur.cur.x, cur.cur.y, cur.cur.z, cur.cur.w};
     const float ol_[4] = {cur.old.x, cur.old.y, cur.old.z, cur.old.w};
     const float ad_[4] = {cur.adv.x, cur.adv.y, cur.adv.z, cur.adv.w};
     const float wv_[4] = {cur.w.x, cur.w.y, cur.w.z, cur.w.w};
-    const bool full = p.vec && i0 + kPpoTpl <= p.n;
+    const bool full = decltype(full_tag)::value || (p.vec && i0 + kPpoTpl <= p.n);
 
     // fast tokens: |delta| <= 2^-2 (finite): the short (|delta| <= 2^-6) and the mid contract
     // series in one lock-step Horner chain per token (k3_small_or_mid), e^delta = (1 + delta) + K3.
-    double dv[kPpoTpl], df[kPpoTpl], k3f[kPpoTpl];
+    // A slow token (|delta| > 2^-2, non-finite) runs the chain too; every result of it is masked
+    // out of the sums below and overwritten by the slow path.
+    double dv[kPpoTpl], k3f[kPpoTpl];
     unsigned slow = full ? 0u : 0xFu;
     if (p.tok_begin + i0 + (kPpoTpl - 1) >= next_b) slow = 0xFu;
 #pragma unroll
@@ -140,22 +176,18 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
       dv[k] = __dsub_rn(static_cast<double>(cu_[k]), static_cast<double>(ol_[k]));
       const bool fast = fabs(dv[k]) <= kMid;  // false for NaN / inf
       if (!fast) slow |= 1u << k;
-      df[k] = fast ? dv[k] : 0.0;
     }
 #pragma unroll
-    for (int k = 0; k < kPpoTpl; ++k) k3f[k] = k3_small_or_mid(df[k], fabs(df[k]) <= kSmall);
+    for (int k = 0; k < kPpoTpl; ++k) k3f[k] = k3_small_or_mid(dv[k], fabs(dv[k]) <= kSmall);
 
     float l_out[kPpoTpl], g_out[kPpoTpl];
     uint32_t cbits = 0;
     double loss_[kPpoTpl], r_[kPpoTpl];
 #pragma unroll
     for (int k = 0; k < kPpoTpl; ++k) {
-      const double d = df[k];
-      const double r = exp_from_k3_small(d, k3f[k]);
-      const double A = static_cast<double>(ad_[k]);
-      const bool clipped = (A > 0.0 && r > p.clip_hi) || (A < 0.0 && r < p.clip_lo);
-      const double sv = clipped ? __dmul_rn(A > 0.0 ? p.clip_hi : p.clip_lo, A) : __dmul_rn(r, A);
-      const double loss = -__dmul_rn(static_cast<double>(wv_[k]), sv);
+      const double r = exp_from_k3_small(dv[k], k3f[k]);
+      bool clipped;
+      const double loss = ppo_token_loss(p, r, static_cast<double>(ad_[k]), wv_[k], clipped);
       if (!(fabs(loss) <= kPpoFastLoss)) slow |= 1u << k;
       const float lf = __double2float_rn(loss);
       l_out[k] = lf;
@@ -174,11 +206,13 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
       for (int k = 0; k < kPpoTpl; ++k) {
         const double A = static_cast<double>(ad_[k]);
         cl += __double2ll_rn(__dmul_rn(loss_[k], kTwo52));
-        ck1 += __double2ll_rn(__dmul_rn(-df[k], kTwo52));
+        ck1 += __double2ll_rn(__dmul_rn(-dv[k], kTwo52));
         ck3 += __double2ll_rn(__dmul_rn(k3f[k], kTwo52));
         ccl += (cbits >> (8 * k)) & 1u;
-        if (A == 0.0) cz += 1u;
-        else atomicAdd(&sh_hist[(A > 0.0 ? 0 : nslot) + hist_slot(p, r_[k], A)], 1);
+        cz += A == 0.0 ? 1u : 0u;
+        const int hs = hist_slot(p, r_[k], A);  // computed for every token: no branch
+        const int slot = A == 0.0 ? 2 * nslot + lane : (A > 0.0 ? 0 : nslot) + hs;
+        atomicAdd(&sh_hist[slot], 1);  // A = 0: the lane's sink slot
       }
       cn = kPpoTpl;
     } else {
@@ -187,7 +221,7 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
         const double A = static_cast<double>(ad_[k]);
         const bool use = wv_[k] != 0.f && !((slow >> k) & 1u);
         const double lz = use ? loss_[k] : 0.0;
-        const double dz = use ? df[k] : 0.0;
+        const double dz = use ? dv[k] : 0.0;
         const double kz = use ? k3f[k] : 0.0;
         cl += __double2ll_rn(__dmul_rn(lz, kTwo52));
         ck1 += __double2ll_rn(__dmul_rn(-dz, kTwo52));
@@ -195,14 +229,14 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
         cn += use ? 1u : 0u;
         ccl += (use && ((cbits >> (8 * k)) & 1u)) ? 1u : 0u;
         cz += (use && A == 0.0) ? 1u : 0u;
-        if (use && A != 0.0) atomicAdd(&sh_hist[(A > 0.0 ? 0 : nslot) + hist_slot(p, r_[k], A)], 1);
+        const int slot = (A > 0.0 ? 0 : nslot) + hist_slot(p, r_[k], A);
+        if (use && A != 0.0) atomicAdd(&sh_hist[slot], 1);
       }
     }
-    s_loss += cl;
     acc.x += cl;
     acc.t += cn;
-    s_k1 += ck1;
-    s_k3 += ck3;
+    f_k1 += ck1;
+    f_k3 += ck3;
     c_contrib += cn;
     c_clip += ccl;
     c_zero += cz;
@@ -217,6 +251,7 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
         const double d = dv[k];
         while (g >= next_b && acc.sid + 1 < p.n_seq) {  // leave the sequence(s) walked past (bounded)
           flush_seq(p.seqp, acc);
+          s_loss += acc.x;
           acc.x = 0;
           acc.t = 0;
           acc.nsat = 0;
@@ -236,9 +271,8 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
         const double k3 = k3_c(d);
         const double r = exp_c(d);
         const double A = static_cast<double>(ad_[k]);
-        const bool clipped = (A > 0.0 && r > p.clip_hi) || (A < 0.0 && r < p.clip_lo);
-        const double sv = clipped ? __dmul_rn(A > 0.0 ? p.clip_hi : p.clip_lo, A) : __dmul_rn(r, A);
-        const double loss = -__dmul_rn(static_cast<double>(wv_[k]), sv);
+        bool clipped;
+        const double loss = ppo_token_loss(p, r, A, wv_[k], clipped);
         l_out[k] = __double2float_rn(loss);
         g_out[k] = clipped ? 0.f : l_out[k];
         cbits = (cbits & ~(0xffu << (8 * k))) | (static_cast<uint32_t>(clipped) << (8 * k));
@@ -250,7 +284,6 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
         c_contrib += 1;
         c_clip += clipped ? 1u : 0u;
         c_sat += sat ? 1u : 0u;
-        s_loss += X;
         s_k1 += X1;
         s_k3 += X3;
         acc.x += X;
@@ -296,23 +329,25 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
       cp_async_16_hint(d, p.cur + i, pol);
       cp_async_16_hint(d + 512, p.old + i, pol);
       cp_async_16_hint(d + 1024, p.adv + i, pol);
-      if (p.coeff) cp_async_16_hint(d + 1536, p.coeff + i, pol);
-      else if (p.resp) cp_async_4(ring4 + j * kPpoStageBytes, p.resp + i);
+      if (kW == kWCoeff) cp_async_16_hint(d + 1536, p.coeff + i, pol);
+      else if (kW == kWResp) cp_async_4(ring4 + j * kPpoStageBytes, p.resp + i);
     }
     cp_async_commit();
   };
   for (int j = 0; j < kPpoStages; ++j) issue(j, c_begin + j);
   int j = 0;
-  for (long long ch = c_begin; ch < c_mid; ++ch) {
+  for (long long cb = c_begin; cb < c_mid; cb += kPpoFold) {
+  const long long ce = cb + kPpoFold < c_mid ? cb + kPpoFold : c_mid;
+  for (long long ch = cb; ch < ce; ++ch) {
     cp_async_wait<kPpoStages - 1>();  // this lane's copies of chunk ch have landed
     const uint8_t* st = ring + j * kPpoStageBytes;
     PpoChunk c;
     c.cur = *reinterpret_cast<const float4*>(st + lane * 16);
     c.old = *reinterpret_cast<const float4*>(st + 512 + lane * 16);
     c.adv = *reinterpret_cast<const float4*>(st + 1024 + lane * 16);
-    if (p.coeff) {
+    if (kW == kWCoeff) {
       c.w = *reinterpret_cast<const float4*>(st + 1536 + lane * 16);
-    } else if (p.resp) {
+    } else if (kW == kWResp) {
       const uint32_t m = *reinterpret_cast<const uint32_t*>(st + 1536 + lane * 4);
       c.w = make_float4((m & 0xffu) ? 1.f : 0.f, (m & 0xff00u) ? 1.f : 0.f, (m & 0xff0000u) ? 1.f : 0.f,
                         (m & 0xff000000u) ? 1.f : 0.f);
@@ -321,12 +356,16 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
     }
     issue(j, ch + kPpoStages);  // the lane has read stage j: refill it
     if (++j == kPpoStages) j = 0;
-    body(c, ch * kPpoWarpTok + lane * kPpoTpl);
+    body(c, ch * kPpoWarpTok + lane * kPpoTpl, std::true_type{});
+  }
+  fold();
   }
   for (long long ch = c_mid; ch < c_end; ++ch) {
     const long long i0 = ch * kPpoWarpTok + lane * kPpoTpl;
-    body(ppo_load(p, i0), i0);
+    body(ppo_load<kW>(p, i0), i0, std::false_type{});
   }
+  fold();
+  s_loss += acc.x;  // this lane's open segment
   // the open sequence segments of the warp (ids are non-decreasing in lane order)
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
@@ -460,19 +499,21 @@ cudaError_t launch_ppo_local(const PpoLocalParams& p, int num_sms, cudaStream_t 
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   const size_t smem = ppo_hist_bytes(p.bins) + static_cast<size_t>(kPpoThreads / 32) * kPpoStages * kPpoStageBytes;
-  if (smem > 48 * 1024) {  // the attribute is per device: set it for the current one
-    static std::atomic<bool> attr_set[kMaxDevices];
+  const int mode = p.coeff ? kWCoeff : (p.resp ? kWResp : kWNone);
+  auto kern = mode == kWCoeff ? ppo_local_kernel<kWCoeff> : (mode == kWResp ? ppo_local_kernel<kWResp> : ppo_local_kernel<kWNone>);
+  if (smem > 48 * 1024) {  // the attribute is per device and kernel: set it for the current device
+    static std::atomic<bool> attr_set[3][kMaxDevices];
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
-    if (!attr_set[dev].load()) {
-      e = cudaFuncSetAttribute(ppo_local_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (!attr_set[mode][dev].load()) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       if (e != cudaSuccess) return e;
-      attr_set[dev].store(true);
+      attr_set[mode][dev].store(true);
     }
   }
-  ppo_local_kernel<<<static_cast<int>(blocks), kPpoThreads, smem, stream>>>(p);
+  kern<<<static_cast<int>(blocks), kPpoThreads, smem, stream>>>(p);
   return cudaGetLastError();
 }
 

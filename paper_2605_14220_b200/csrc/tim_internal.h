@@ -202,6 +202,7 @@ struct PpoLocalParams {
   int64_t tok_begin;
   int64_t n;
   double clip_lo, clip_hi, hist_lo, hist_inv_width;
+  double bins_d;         // (double) bins, for the branch-free histogram slot
   int bins;
   float* loss;
   float* grad;

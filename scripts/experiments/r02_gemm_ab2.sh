@@ -1,7 +1,7 @@
 #!/bin/bash
 mkdir -p gpurun_out
 export PYTHONPATH=$PWD
-timeout -s KILL 400 python scripts/gemm_knob_ab.py 2048 > gpurun_out/gemm_knob_2048.txt 2>&1
+timeout -s KILL 400 python scripts/experiments/gemm_knob_ab.py 2048 > gpurun_out/gemm_knob_2048.txt 2>&1
 for v in "0 1 1 2 3" "128 1 1 2 3" "128 1 1 1 3" "32 1 1 1 3"; do
 set -- $v
 timeout -s KILL 300 ncu --metrics gpu__time_duration.sum,sm__cycles_elapsed.avg.per_second,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,dram__bytes_write.sum,dram__bytes_read.sum,lts__t_sector_hit_rate.pct --clock-control none --csv -k regex:bwd_gemm \
