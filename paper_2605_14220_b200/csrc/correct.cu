@@ -383,9 +383,15 @@ __device__ __forceinline__ void fast_body(const LocalParams& p, LaneState& st, F
       fa.ab = __dadd_rn(fa.ab, fabs(x1));
       if (kSeq) fa.seq = __dadd_rn(fa.seq, seq_k1 ? x1 : x3);
     }
-    const double a01 = fmax(fabs(ds[0]), fabs(ds[1]));
-    const double a23 = fmax(fabs(ds[2]), fabs(ds[3]));
-    fa.mx = fmax(fa.mx, fmax(a01, a23));
+    // running max |delta| as compare-and-select (ds is never NaN here, so fmax's NaN handling --
+    // five instructions per step -- is not needed; the same value results)
+    double amx = fa.mx;
+#pragma unroll
+    for (int k = 0; k < kTpl; ++k) {
+      const double a = fabs(ds[k]);
+      amx = a > amx ? a : amx;
+    }
+    fa.mx = amx;
     fa.resp += kTpl;
     if (kSeq) fa.seq_t += kTpl;
   }

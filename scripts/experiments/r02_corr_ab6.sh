@@ -1,6 +1,6 @@
 #!/bin/bash
-# Round 2 (late): correction pass 1 with running source pointers for the cp.async issue and the
-# fp64 sums folded per block of 16 chunks (libtim.so) vs the previous build (libtim_old.so);
+# Round 2 (late): correction pass 1 variants (libtim.so) vs the previous build (libtim_old.so);
+# variant 3: the running max |delta| of the fast body as compare-and-select (no fmax NaN handling);
 # correction parity first, then interleaved end-to-end timing at 2^27 tokens.
 mkdir -p gpurun_out
 timeout -s KILL 1200 python -m pytest tests/test_gpu_correct.py tests/test_gpu_correct_paths.py tests/test_gpu_sweep.py tests/test_gpu_robustness.py -m gpu -q -x > gpurun_out/corr_tests.log 2>&1; echo tests_rc=$?; tail -2 gpurun_out/corr_tests.log
