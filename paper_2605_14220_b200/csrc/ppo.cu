@@ -153,6 +153,8 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
     acc.sid = seq_of(p.cu, p.n_seq, p.tok_begin + c_begin * kPpoWarpTok + lane * kPpoTpl);
     next_b = __ldg(p.cu + acc.sid + 1);
   }
+  // i0 >= seq_lim <=> the lane's tokens reach the start of the next sequence
+  long long seq_lim = next_b - p.tok_begin - (kPpoTpl - 1);
 
   if (blockIdx.x == 0 && threadIdx.x == 0) shard_range_check(p.cu, p.n_seq, p.tok_begin, p.n, bad_inv);
 
@@ -168,14 +170,14 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
     // series in one lock-step Horner chain per token (k3_small_or_mid), e^delta = (1 + delta) + K3.
     // A slow token (|delta| > 2^-2, non-finite) runs the chain too; every result of it is masked
     // out of the sums below and overwritten by the slow path.
+    // The slow decision is per lane: one slow token sends the lane's four tokens to the slow path
+    // (rare, and the slow path is the full contract, so the results are the same).
     double dv[kPpoTpl], k3f[kPpoTpl];
-    unsigned slow = full ? 0u : 0xFu;
-    if (p.tok_begin + i0 + (kPpoTpl - 1) >= next_b) slow = 0xFu;
+    bool lane_slow = !full || i0 >= seq_lim;
 #pragma unroll
     for (int k = 0; k < kPpoTpl; ++k) {
       dv[k] = __dsub_rn(static_cast<double>(cu_[k]), static_cast<double>(ol_[k]));
-      const bool fast = fabs(dv[k]) <= kMid;  // false for NaN / inf
-      if (!fast) slow |= 1u << k;
+      lane_slow |= !(fabs(dv[k]) <= kMid);  // true for NaN / inf
     }
 #pragma unroll
     for (int k = 0; k < kPpoTpl; ++k) k3f[k] = k3_small_or_mid(dv[k], fabs(dv[k]) <= kSmall);
@@ -188,7 +190,7 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
       const double r = exp_from_k3_small(dv[k], k3f[k]);
       bool clipped;
       const double loss = ppo_token_loss(p, r, static_cast<double>(ad_[k]), wv_[k], clipped);
-      if (!(fabs(loss) <= kPpoFastLoss)) slow |= 1u << k;
+      lane_slow |= !(fabs(loss) <= kPpoFastLoss);
       const float lf = __double2float_rn(loss);
       l_out[k] = lf;
       g_out[k] = clipped ? 0.f : lf;
@@ -196,6 +198,7 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
       loss_[k] = loss;
       r_[k] = r;
     }
+    const unsigned slow = lane_slow ? 0xFu : 0u;
     long long cl = 0, ck1 = 0, ck3 = 0;  // chunk sums: |X| <= 2^60 (loss), 2^52 (K1, K3)
     unsigned cn = 0, ccl = 0, cz = 0;
     // warp-uniform: every token of the chunk fast and weighted (the common case inside the
@@ -257,6 +260,7 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
           acc.nsat = 0;
           acc.sid += 1;
           next_b = __ldg(p.cu + acc.sid + 1);
+          seq_lim = next_b - p.tok_begin - (kPpoTpl - 1);
         }
         // data error (U13): a non-finite log-prob, advantage or weight -- loss NaN, grad 0, the
         // token excluded from the histogram and every sum
