@@ -100,3 +100,53 @@ def test_ppo_nan_status(tim):
     st = new_status(DEV)
     res = tim.ppo_loss(cur.to(DEV), old.to(DEV), adv.to(DEV), cu.to(DEV), tim.PPOConfig(), status=st)
     assert read_status(st) == (9, 777) and math.isnan(res["loss"][777].item())
+
+
+@pytest.mark.parametrize("wmode", ["coeff", "mask", "none"])
+def test_ppo_lock_step_edges_bit_exact(tim, wmode):
+    """The lock-step path's edges (csrc/ppo.cu): a single slow token inside an otherwise clean
+    128-token chunk (|delta| just above / at 2^-2, |loss| just above 2^8, a non-finite advantage),
+    A = 0 tokens (the per-lane sink slot of the C(r) histogram), C(r) below / above the histogram
+    range and exactly on a bin edge, tokens clipped on both sides, sequence starts inside a lane's
+    four tokens; every weight source (coefficient / response mask / none: three kernel
+    instantiations).  Element-wise bit-exact against oracle/ppo.py."""
+    from paper_2605_14220_b200.tim import new_status, read_status
+    L = 128 * 6
+    cu = torch.tensor([0, 130, 131, 640, 2 * L - 5, 2 * L, 3 * L], dtype=torch.int64)  # starts inside lanes
+    N = int(cu[-1])
+    g = torch.Generator().manual_seed(90 + len(wmode))
+    old = -torch.empty(N).exponential_(0.7, generator=g)
+    cur = synth.policy_move(old, 91, sd=0.03)
+    adv = torch.randn(N, generator=g)
+    d = torch.zeros(N)
+    d[200], d[333], d[1000] = 0.25, 0.2500001, -0.75      # |delta| at / above the fast bound, large
+    cur[200], cur[333], cur[1000] = old[200] + d[200], old[333] + d[333], old[1000] + d[1000]
+    adv[444] = 300.0                                       # |loss| > 2^8 on a fast delta
+    adv[445] = 0.0
+    adv[512:640] = 0.0                                     # a whole chunk of A = 0
+    cur[700], adv[700] = old[700] + 0.5, 1.0               # clipped high
+    cur[701], adv[701] = old[701] - 0.5, -1.0              # clipped low
+    cur[702], adv[702] = old[702], 0.25                    # r = 1 exactly: C = 0 on a bin edge
+    cur[703], adv[703] = old[703] - 0.2, 100.0             # C far above the range
+    cur[704], adv[704] = old[704] + 0.2, 100.0             # C far below the range
+    cfg = tim.PPOConfig(eps=0.2, hist_lo=-0.5, hist_hi=0.5, hist_bins=40)
+    mask = synth.resp_mask(cu, 7)
+    coeff = (torch.rand(N, generator=g) * 2).float() * mask.float()
+    kw, okw = {}, {}
+    if wmode == "coeff":
+        kw, okw = {"coeff": coeff.to(DEV)}, {"coeff": coeff.numpy()}
+    elif wmode == "mask":
+        kw, okw = {"resp_mask": mask.to(DEV)}, {"resp_mask": mask.numpy()}
+    res = tim.ppo_loss(cur.float().to(DEV), old.float().to(DEV), adv.float().to(DEV), cu.to(DEV), cfg, **kw)
+    ref = op.ppo(cur.float().numpy(), old.float().numpy(), adv.float().numpy(), cu.numpy(), _ocfg(cfg), **okw)
+    _compare(res, ref)
+    # a non-finite advantage inside a clean chunk: data error, token excluded, the rest unchanged
+    adv2 = adv.clone()
+    adv2[900] = float("inf")
+    st = new_status(DEV)
+    res2 = tim.ppo_loss(cur.float().to(DEV), old.float().to(DEV), adv2.float().to(DEV), cu.to(DEV), cfg,
+                        status=st, **kw)
+    assert read_status(st) == (9, 900)
+    keep = torch.ones(N, dtype=torch.bool)
+    keep[900] = False
+    assert torch.equal(res2["loss"].cpu()[keep].view(torch.int32), res["loss"].cpu()[keep].view(torch.int32))
