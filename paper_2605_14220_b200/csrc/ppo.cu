@@ -29,6 +29,12 @@ constexpr int kPpoWarpTok = 32 * kPpoTpl;
 #ifndef TIM_PPO_MINB
 #define TIM_PPO_MINB 4
 #endif
+#ifndef TIM_PPO_PLAIN_STORES
+#define TIM_PPO_PLAIN_STORES 0  // 1: plain stores instead of st.global.cs (0.7% slower here)
+#endif
+#ifndef TIM_PPO_LOAD_HINT
+#define TIM_PPO_LOAD_HINT 0  // 1: cp.async reads with an L2 evict_first policy (0.6% slower)
+#endif
 #ifndef TIM_PPO_STAGES
 #define TIM_PPO_STAGES 4
 #endif
@@ -299,9 +305,15 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
     }
 
     if (full) {
+#if TIM_PPO_PLAIN_STORES
+      *reinterpret_cast<float4*>(p.loss + i0) = make_float4(l_out[0], l_out[1], l_out[2], l_out[3]);
+      *reinterpret_cast<float4*>(p.grad + i0) = make_float4(g_out[0], g_out[1], g_out[2], g_out[3]);
+      *reinterpret_cast<unsigned int*>(p.clipped + i0) = cbits;
+#else
       __stcs(reinterpret_cast<float4*>(p.loss + i0), make_float4(l_out[0], l_out[1], l_out[2], l_out[3]));
       __stcs(reinterpret_cast<float4*>(p.grad + i0), make_float4(g_out[0], g_out[1], g_out[2], g_out[3]));
       __stcs(reinterpret_cast<unsigned int*>(p.clipped + i0), cbits);
+#endif
     } else {
 #pragma unroll
       for (int k = 0; k < kPpoTpl; ++k) {
@@ -325,15 +337,22 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
   uint8_t* ring = reinterpret_cast<uint8_t*>(sh_hist) + ppo_hist_bytes(p.bins) + wib * kPpoStages * kPpoStageBytes;
   const uint32_t ring16 = smem_u32(ring) + lane * 16;
   const uint32_t ring4 = smem_u32(ring) + 3 * 512 + lane * 4;
-  const uint64_t pol = policy_evict_first();
+  [[maybe_unused]] const uint64_t pol = policy_evict_first();
   auto issue = [&](int j, long long c) {  // chunk c into stage j (one commit group, possibly empty)
     if (c < c_mid) {
       const long long i = c * kPpoWarpTok + lane * kPpoTpl;
       const uint32_t d = ring16 + j * kPpoStageBytes;
+#if TIM_PPO_LOAD_HINT
       cp_async_16_hint(d, p.cur + i, pol);
       cp_async_16_hint(d + 512, p.old + i, pol);
       cp_async_16_hint(d + 1024, p.adv + i, pol);
       if (kW == kWCoeff) cp_async_16_hint(d + 1536, p.coeff + i, pol);
+#else
+      cp_async_16(d, p.cur + i);
+      cp_async_16(d + 512, p.old + i);
+      cp_async_16(d + 1024, p.adv + i);
+      if (kW == kWCoeff) cp_async_16(d + 1536, p.coeff + i);
+#endif
       else if (kW == kWResp) cp_async_4(ring4 + j * kPpoStageBytes, p.resp + i);
     }
     cp_async_commit();
