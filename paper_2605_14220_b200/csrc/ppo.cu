@@ -46,6 +46,10 @@ constexpr int kMaxHistBins = 1024;
 constexpr long long kPpoFold = 1024;       // chunks per int64 K1 / K3 fold: 2^10 x 2^52 < 2^63
 constexpr double kPpoFastLoss = 256.0;      // fast path: |loss| <= 2^8, so |X| <= 2^60 and four fit int64
 
+struct PpoCold {
+  __int128 s_loss, s_k1, s_k3;
+};
+
 struct PpoChunk {
   float4 cur, old, adv, w;  // w = coeff, or the response mask as 0 / 1
 };
@@ -139,11 +143,17 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
   // s_loss collects each flushed sequence segment (acc.x), so the hot path adds the chunk's loss
   // once (to acc.x); the lock-step path's K1 / K3 chunk sums (|X| <= 2^52 per chunk) go to int64
   // lane accumulators folded into the int128 sums every kPpoFold chunks.
-  __int128 s_loss = 0, s_k1 = 0, s_k3 = 0;
+  // the int128 sums are touched only at folds, flushes and in the slow path: per-thread shared
+  // memory, so the hot loop keeps its registers
+  __shared__ PpoCold sh_cold[kPpoThreads];
+  PpoCold& cold = sh_cold[threadIdx.x];
+  cold.s_loss = 0;
+  cold.s_k1 = 0;
+  cold.s_k3 = 0;
   long long f_k1 = 0, f_k3 = 0;
   auto fold = [&]() {
-    s_k1 += f_k1;
-    s_k3 += f_k3;
+    cold.s_k1 += f_k1;
+    cold.s_k3 += f_k3;
     f_k1 = 0;
     f_k3 = 0;
   };
@@ -260,7 +270,7 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
         const double d = dv[k];
         while (g >= next_b && acc.sid + 1 < p.n_seq) {  // leave the sequence(s) walked past (bounded)
           flush_seq(p.seqp, acc);
-          s_loss += acc.x;
+          cold.s_loss += acc.x;
           acc.x = 0;
           acc.t = 0;
           acc.nsat = 0;
@@ -294,8 +304,8 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
         c_contrib += 1;
         c_clip += clipped ? 1u : 0u;
         c_sat += sat ? 1u : 0u;
-        s_k1 += X1;
-        s_k3 += X3;
+        cold.s_k1 += X1;
+        cold.s_k3 += X3;
         acc.x += X;
         acc.t += 1;
         acc.nsat += sat ? 1 : 0;
@@ -388,7 +398,8 @@ __global__ void __launch_bounds__(kPpoThreads, kPpoMinB) ppo_local_kernel(PpoLoc
     body(ppo_load<kW>(p, i0), i0, std::false_type{});
   }
   fold();
-  s_loss += acc.x;  // this lane's open segment
+  __int128 s_loss = cold.s_loss + acc.x;  // + this lane's open segment
+  __int128 s_k1 = cold.s_k1, s_k3 = cold.s_k3;
   // the open sequence segments of the warp (ids are non-decreasing in lane order)
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
