@@ -13,10 +13,27 @@ if len(sys.argv) > 2:
     tim.debug_set_tuning(0, 0, 0, int(sys.argv[2]))
 if os.environ.get("TUN"):  # h_policy,w_policy,sleep_waits,sync_slack
     tim.debug_set_tuning(*[int(x) for x in os.environ["TUN"].split(",")])
+if os.environ.get("PERSIST") or os.environ.get("QUERY"):
+    # cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, PERSIST MB); QUERY=1 only prints it
+    import ctypes
+    torch.cuda.init()
+    torch.empty(1, device="cuda")  # the primary context exists before the limit is set
+    rt = ctypes.CDLL("libcudart.so.12")
+    lim0 = ctypes.c_size_t(0)
+    rt.cudaDeviceGetLimit(ctypes.byref(lim0), 6)
+    print(f"persisting L2 limit before: {lim0.value} B")
+if os.environ.get("PERSIST"):
+    mx = ctypes.c_int(0)
+    rt.cudaDeviceGetAttribute(ctypes.byref(mx), 108, 0)  # cudaDevAttrMaxPersistingL2CacheSize
+    want = min(int(os.environ["PERSIST"]) << 20, mx.value)
+    err = rt.cudaDeviceSetLimit(6, ctypes.c_size_t(want))  # cudaLimitPersistingL2CacheSize
+    lim = ctypes.c_size_t(0)
+    rt.cudaDeviceGetLimit(ctypes.byref(lim), 6)
+    print(f"persisting L2 limit: max {mx.value >> 20} MB, set {want >> 20} MB, err {err}, now {lim.value >> 20} MB")
 if os.environ.get("DEMOTE"):
     tim.debug_set_schedule(0, os.environ["DEMOTE"] == "1")
 dev = torch.device("cuda")
-cfg = synth.CONFIGS["c2"]
+cfg = synth.CONFIGS[os.environ.get("CFG", "c2")]
 W, H, ids, tb, cu, mask, n_glob = bench.build_workload(cfg, "strong", 1, 0, dev)
 N = H.shape[0]
 lp = torch.empty(N, device=dev)
