@@ -234,7 +234,7 @@ def logprob(hidden: torch.Tensor, weight: torch.Tensor, ids: torch.Tensor, tempe
     return lp, ent
 
 
-_HOST_CHUNK = int(os.environ.get("TIM_HOST_CHUNK", 65536))  # rows per host->device chunk (multiple of 256)
+_HOST_CHUNK = int(os.environ.get("TIM_HOST_CHUNK", 524288))  # rows per host->device chunk (multiple of 256)
 _HOST_FIRST = 8192           # the first chunks ramp up 8k, 16k, 32k: only a small copy is exposed
 _copy_streams: dict = {}
 
