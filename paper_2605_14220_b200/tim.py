@@ -196,7 +196,7 @@ def logprob(hidden: torch.Tensor, weight: torch.Tensor, ids: torch.Tensor, tempe
     """
     host = not hidden.is_cuda
     dev = torch.device(device) if device is not None else (hidden.device if not host else torch.device("cuda"))
-    if host and out is None and hidden.shape[0] >= 2 * _HOST_CHUNK:
+    if host and out is None and hidden.shape[0] >= 4 * _HOST_FIRST:
         return _logprob_from_host(hidden, weight, ids, temperature, temperatures, entropy, status, dev)
     if host:
         hidden = hidden.to(dev, non_blocking=True)
