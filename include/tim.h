@@ -466,6 +466,18 @@ tim_status tim_ppo_finish(const void* gathered_partials, int32_t nranks, int64_t
 tim_status tim_ppo_stats_finalize(tim_ppo_stats* host_copy);
 
 /* ----------------------------------------------------------------------------
+ * Device L2 configuration (an application-level setting, never changed by any other call).
+ * tim_l2_persisting: set the current device's persisting-L2 set-aside (cudaLimitPersistingL2CacheSize)
+ * to min(bytes, the device maximum) and return the size the driver granted (it rounds up; 79 MB max
+ * on B200).  The log-prob kernels load their live H tiles with the evict_last L2 policy; on boxes
+ * whose C2 launches fall into the slow mode (W re-fetched) a ~48 MB set-aside kept every
+ * launch in the fast mode, and it measured neutral elsewhere (profiles/r02_c2_bimodal.txt).  The
+ * limit is context-wide: it also shrinks the L2 left to normal accesses of every other kernel in the
+ * process.  bytes < 0: TIM_ERR_VALUE; a CUDA failure: TIM_ERR_CUDA.  granted_bytes may be NULL.
+ * -------------------------------------------------------------------------- */
+tim_status tim_l2_persisting(int64_t bytes, int64_t* granted_bytes);
+
+/* ----------------------------------------------------------------------------
  * NCCL communicator (NVLink / NVSwitch).  libnccl.so.2 is loaded at run time.
  * unique_id: 128 bytes from tim_comm_unique_id on rank 0, broadcast by the caller.
  * -------------------------------------------------------------------------- */

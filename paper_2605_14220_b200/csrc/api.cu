@@ -853,6 +853,21 @@ tim_status tim_comm_destroy(tim_comm* comm) {
 }
 
 // ------------------------------------------------ vocab-parallel (TP) head (NEXT-4) --
+tim_status tim_l2_persisting(int64_t bytes, int64_t* granted_bytes) {
+  if (bytes < 0) return TIM_ERR_VALUE;
+  int dev = 0, mx = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess)
+    return TIM_ERR_CUDA;
+  const size_t want = static_cast<size_t>(bytes < mx ? bytes : mx);
+  size_t got = 0;
+  if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess ||
+      cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize) != cudaSuccess)
+    return TIM_ERR_CUDA;
+  if (granted_bytes) *granted_bytes = static_cast<int64_t>(got);
+  return TIM_OK;
+}
+
 tim_status tim_tp_vocab_range(int32_t vocab, int32_t tp, int32_t rank, int32_t* begin, int32_t* end) {
   if (!begin || !end) return TIM_ERR_NULL;
   if (vocab < 1 || tp < 1 || rank < 0 || rank >= tp) return TIM_ERR_SHAPE;

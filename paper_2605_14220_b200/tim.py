@@ -79,6 +79,7 @@ _SIGS = {
     "tim_correct_local": (_I32, [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "tim_correct_finish": (_I32, [_P, _I32, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P]),
     "tim_tp_vocab_range": (_I32, [_I32, _I32, _I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
+    "tim_l2_persisting": (_I32, [ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]),
     "tim_logprob_tp_partial_bytes": (_SZ, [_I64, _I32, _I32]),
     "tim_logprob_tp_partial": (_I32, [_P, _I64, _P, _I32, _I32, _I32, _I32, _P, _I64, _F, _P, _P, _P, _SZ, _P]),
     "tim_logprob_tp_merge": (_I32, [_P, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _P, _P]),
@@ -304,6 +305,15 @@ def sample(hidden: torch.Tensor, weight: torch.Tensor, row_keys: torch.Tensor, s
                         ctypes.c_uint64(int(seed) % (1 << 64)), float(temperature), _ptr(temperatures), _ptr(ids),
                         _ptr(lp), _ptr(ent), _ptr(ws), ws.numel(), _ptr(status), _stream(dev)), "tim_sample")
     return ids, lp, ent
+
+
+def l2_persisting(nbytes: int, device=None) -> int:
+    """tim_l2_persisting: the device's persisting-L2 set-aside (application-level; see include/tim.h).
+    Returns the granted size in bytes."""
+    got = ctypes.c_int64(0)
+    with torch.cuda.device(device if device is not None else torch.cuda.current_device()):
+        _check(lib().tim_l2_persisting(int(nbytes), ctypes.byref(got)), "tim_l2_persisting")
+    return int(got.value)
 
 
 def tp_vocab_range(vocab: int, tp: int, rank: int) -> tuple[int, int]:

@@ -213,3 +213,8 @@ def test_tp_partial_rejects_a_shard_of_the_wrong_split():
         tim.logprob_tp_partial(H, torch.zeros(e - b, d + 64, dtype=torch.bfloat16), V, tp, 0, ids)
     with pytest.raises(TypeError):
         tim.logprob_tp_partial(H, torch.zeros(e - b, d, dtype=torch.float32), V, tp, 0, ids)
+
+
+def test_l2_persisting_rejects_negative_size_before_any_cuda_call(L):
+    L.tim_l2_persisting.argtypes = [ctypes.c_int64, ctypes.c_void_p]
+    assert L.tim_l2_persisting(-1, None) == 4     # TIM_ERR_VALUE, no device touched

@@ -130,3 +130,21 @@ def test_two_streams_do_not_share_a_workspace(tim):
     for got, (_, _, ref) in zip((a, b), out):
         assert torch.equal(got[0].view(torch.int32), ref[0].view(torch.int32))
         assert torch.equal(got[1].view(torch.int32), ref[1].view(torch.int32))
+
+
+def test_l2_persisting_set_aside(tim):
+    """tim_l2_persisting (application-level L2 setup used by bench.py): the driver grants at least the
+    request up to the device maximum (rounding up), 0 clears it, and a log-prob call after either
+    setting gives the same bits (the set-aside is a cache policy, never a result)."""
+    import synth
+    W = synth.head_weight(3000, 256, 5, device="cuda")
+    ids = synth.token_ids(700, 3000, 5, device="cuda")
+    H = synth.hidden_states(700, 256, 5, device="cuda", weight=W, ids=ids, mode="peaked")
+    g = tim.l2_persisting(48 << 20)
+    assert g >= 48 << 20
+    a = tim.logprob(H, W, ids)
+    assert tim.l2_persisting(0) == 0
+    b = tim.logprob(H, W, ids)
+    assert torch.equal(a[0].view(torch.int32), b[0].view(torch.int32))
+    assert tim.l2_persisting(1 << 40) == tim.l2_persisting(1 << 41)   # clamped to the device maximum
+    tim.l2_persisting(0)
