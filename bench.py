@@ -698,8 +698,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--l2-persist-mb", type=int, default=48,
-                    help="device persisting-L2 set-aside in MB for our arm (-1: leave the driver default)")
+    ap.add_argument("--l2-persist-mb", type=int, default=-1,
+                    help="device persisting-L2 set-aside in MB for our arm (-1: leave the driver default; "
+                         "48 slowed the correction / PPO passes by 27%%, profiles/r02_c2_bimodal.txt)")
     ap.add_argument("--correction-tokens", type=int, default=1 << 27,
                     help="standalone correction-kernel HBM roofline at this many tokens (0 = skip)")
     ap.add_argument("--tuning", default=None,

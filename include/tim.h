@@ -473,7 +473,8 @@ tim_status tim_ppo_stats_finalize(tim_ppo_stats* host_copy);
  * whose C2 launches fall into the slow mode (W re-fetched) a ~48 MB set-aside kept every
  * launch in the fast mode, and it measured neutral elsewhere (profiles/r02_c2_bimodal.txt).  The
  * limit is context-wide: it also shrinks the L2 left to normal accesses of every other kernel in the
- * process.  bytes < 0: TIM_ERR_VALUE; a CUDA failure: TIM_ERR_CUDA.  granted_bytes may be NULL.
+ * process -- with 48 MB the streaming correction / PPO passes ran 27% slower (0.565 -> 0.723 ms and
+ * 0.623 -> 0.794 ms at 2^27 tokens), so bench.py leaves the driver default.  bytes < 0: TIM_ERR_VALUE; a CUDA failure: TIM_ERR_CUDA.  granted_bytes may be NULL.
  * -------------------------------------------------------------------------- */
 tim_status tim_l2_persisting(int64_t bytes, int64_t* granted_bytes);
 
