@@ -31,7 +31,7 @@ tim_status tim_debug_set_pad_small(int32_t enable);
 
 /* Performance knobs (never change results): L2 eviction policy of the hidden-state (H) and
  * weight (W) TMA tile loads, 0 = no hint, 1 = evict_normal, 2 = evict_first, 3 = evict_last;
- * sleep_waits = 1 makes the TMA-producer and epilogue mbarrier waits sleep in hardware;
+ * sleep_waits (bits: 1 TMA producer, 2 epilogue, 4 MMA issuer; 0..7) makes those mbarrier waits sleep in hardware;
  * sync_slack > 0 bounds how many vocab tiles a CTA pair may run ahead of the slowest pair.
  * Defaults: h = 3, w = 2, sleep_waits = 0, sync_slack = 4. */
 tim_status tim_debug_set_tuning(int32_t h_policy, int32_t w_policy, int32_t sleep_waits, int32_t sync_slack);

@@ -1404,10 +1404,11 @@ tim_status tim_debug_set_correct_split(int32_t split) {
 tim_status tim_debug_set_tuning(int32_t h_policy, int32_t w_policy, int32_t sleep_waits, int32_t sync_slack) {
   if (sync_slack < 0) return TIM_ERR_VALUE;
   if (h_policy < 0 || h_policy > 3 || w_policy < 0 || w_policy > 3) return TIM_ERR_VALUE;
+  if (sleep_waits < 0 || sleep_waits > 7) return TIM_ERR_VALUE;
   g_sync_slack = sync_slack;
   g_h_policy = h_policy;
   g_w_policy = w_policy;
-  g_sleep_waits = sleep_waits != 0;
+  g_sleep_waits = sleep_waits;  // bit 0 producer, bit 1 epilogue, bit 2 MMA issuer (3 = the round-1 'sleep')
   return TIM_OK;
 }
 

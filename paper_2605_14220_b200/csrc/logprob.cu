@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int n0 = vt * kTileN - p.w_row0 + prank * C::kBRows + (kNP == 2 ? pid * (C::kBRows / 2) : 0);
         for (int kb = 0; kb < nkb; ++kb) {
-          if (p.sleep_waits) mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
+          if (p.sleep_waits & 1) mbar_wait_sleep(smem_u32(&empty[stage]), phase ^ 1);
           else mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
           if (kPair && kNP == 1 && hints) {
             // the default path, warp-wide: one elected lane issues (no single-lane issue loops)
@@ -477,11 +477,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int k = 0; sched.unit(vcid, k, dm, j); ++k) {
         const int t0 = slice_tile(p, j), t1 = slice_tile(p, j + 1);
         for (int vt = t0; vt < t1; ++vt) {
-          mbar_wait(smem_u32(&tempty[acc]), aphase ^ 1);
+          if (p.sleep_waits & 4) mbar_wait_sleep(smem_u32(&tempty[acc]), aphase ^ 1);
+          else mbar_wait(smem_u32(&tempty[acc]), aphase ^ 1);
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + acc * kTileN;
           for (int kb = 0; kb < nkb; ++kb) {
-            mbar_wait(smem_u32(&full[stage]), phase);
+            if (p.sleep_waits & 4) mbar_wait_sleep(smem_u32(&full[stage]), phase);
+            else mbar_wait(smem_u32(&full[stage]), phase);
             tc_fence_after();
             const uint64_t da = desc_a0 + stage * (C::kABytes >> 4);
             const uint64_t db = desc_b0 + stage * (C::kBBytes >> 4);
@@ -538,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int t0 = slice_tile(p, j), t1 = slice_tile(p, j + 1);
       for (int vt = t0; vt < t1; ++vt) {
-        if (p.sleep_waits) mbar_wait_sleep(smem_u32(&tfull[acc]), aphase);
+        if (p.sleep_waits & 2) mbar_wait_sleep(smem_u32(&tfull[acc]), aphase);
         else mbar_wait(smem_u32(&tfull[acc]), aphase);
         tc_fence_after();
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kTileN;

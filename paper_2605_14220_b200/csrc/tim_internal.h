@@ -41,7 +41,7 @@ struct LogprobParams {
   int64_t debug_ld;
   int h_policy;         // L2 eviction policy of H / W tile loads: 0 none, 1 normal, 2 first, 3 last
   int w_policy;
-  int sleep_waits;      // producer / epilogue mbarrier waits sleep (suspend-time hint) instead of polling
+  int sleep_waits;      // mbarrier waits that sleep (suspend-time hint) instead of polling: bit 0 producer, 1 epilogue, 2 MMA
   uint32_t* progress;   // [clusters] tiles issued per CTA pair (workspace, zeroed per call)
   int sync_slack;       // max tiles a pair may run ahead of the slowest pair (0 = no throttle)
   int group;            // pairs sharing one M-tile (split its slices) so the live H tiles fit in L2

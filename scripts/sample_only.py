@@ -8,7 +8,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 from paper_2605_14220_b200 import tim  # noqa: E402
 
-cfg = synth.CONFIGS["c1"]
+if os.environ.get("TUN"):  # h_policy,w_policy,sleep_waits,sync_slack
+    tim.debug_set_tuning(*[int(x) for x in os.environ["TUN"].split(",")])
+cfg = synth.CONFIGS[os.environ.get("CFG", "c1")]
 W = synth.head_weight(cfg.vocab, cfg.hidden, cfg.seed, device="cuda")
 ids = synth.token_ids(cfg.n_tok, cfg.vocab, cfg.seed, device="cuda")
 H = synth.hidden_states(cfg.n_tok, cfg.hidden, cfg.seed, device="cuda", weight=W, ids=ids, mode="peaked")

@@ -192,6 +192,7 @@ def test_debug_knobs_validate_arguments(L):
     assert L.tim_debug_set_pad_small(2) == 4 and L.tim_debug_set_pad_small(-1) == 4
     assert L.tim_debug_set_pad_small(1) == 0
     assert L.tim_debug_set_tuning(4, 2, 0, 4) == 4 and L.tim_debug_set_tuning(3, 2, 0, -1) == 4
+    assert L.tim_debug_set_tuning(3, 2, 8, 4) == 4          # sleep bits 0..7
     assert L.tim_debug_set_tuning(3, 2, 0, 4) == 0          # the defaults
     assert L.tim_debug_set_kernel(2, 0) == 4 and L.tim_debug_set_kernel(1, -1) == 4
     assert L.tim_debug_set_kernel(1, 0) == 0
